@@ -1,0 +1,209 @@
+/*
+ * medha_attn.h — C ABI of libmedha_attn: the data-parallel hot path of Medha
+ * (arXiv 2409.17264), exact attention over a KV cache sharded along the
+ * sequence dimension, on NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" = PAPER.md line n of the paper's LaTeX source, "S:n" = the
+ * SPEC.md line n written from it (see DESIGN.md for the readings R1-R18 of the
+ * places where the paper is silent).
+ *
+ * What the library computes (P:167-171 attention; P:597-599 KVP):
+ *   for a query row (token t, query head h) with absolute position q_pos[t],
+ *   kv head g = h / G (G = h_q / h_kv, reading R2), and the keys j of a shard
+ *   with absolute position pos0 + j <= q_pos[t] (causal, inclusive, R3):
+ *      z_j = scale * <Q[t,h,:], K[g,j,:]>,  m = max_j z_j,  l = sum_j exp(z_j - m)
+ *      o   = sum_j exp(z_j - m) V[g,j,:] / l,        lse = m + ln(l)   (natural log, R5)
+ *   A row with no visible key gives o = 0, lse = -inf (R7).
+ *   Partials of disjoint shards merge exactly ("combined using online-softmax"):
+ *      M = max_r lse_r, lse = M + ln sum_r exp(lse_r - M), o = sum_r exp(lse_r - lse) o_r,
+ *   summed in rank order r = 0..P-1 so every rank gets bit-identical results (R13).
+ *
+ * Conventions for every entry point:
+ *   - Tensor pointers are DEVICE pointers owned by the caller unless the
+ *     parameter name ends in _host (then: host memory, preferably pinned).
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *     NULL = the legacy default stream), never synchronises the device, and never
+ *     allocates device memory (except medha_kvp_comm_create, through NCCL).
+ *   - Precision (R8): K, V, Q are bf16; logits, softmax, accumulation and all
+ *     outputs are fp32; P is rounded to bf16 (RNE) before the P.V product.
+ *   - Alignment: every device pointer must be 16-byte aligned.
+ *   - Supported shapes: d in {64, 128}; G = h_q / h_kv in {1, 2, 4, 8, 16};
+ *     otherwise MEDHA_ENOTSUP.
+ *   - Errors are returned as a negative medha_status; nothing is launched when
+ *     a call returns an error detected on the host.  medha_last_error() returns a
+ *     thread-local message for the last failing call on the calling thread.
+ *   - Workspaces: caller-owned device memory of at least the size the matching
+ *     *_workspace_size() returns.  They must be ZERO-FILLED before their first
+ *     use; every call leaves the workspace's counter region zeroed again, so a
+ *     workspace can be reused (and captured in a CUDA graph) indefinitely.
+ *     Two calls that run concurrently need distinct workspaces.
+ *   - Thread safety: calls are reentrant for distinct outputs and workspaces.
+ */
+#ifndef MEDHA_ATTN_H_
+#define MEDHA_ATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t medha_status;
+enum {
+  MEDHA_OK = 0,
+  MEDHA_EINVAL = -1,     /* null pointer, misaligned pointer, h_q % h_kv != 0, negative size */
+  MEDHA_ESHAPE = -2,     /* dimensions of the arguments disagree */
+  MEDHA_ERANGE = -3,     /* capacity overflow, bad position, merge of all -inf rows */
+  MEDHA_ENOTSUP = -4,    /* d or G outside the supported set, batch too large */
+  MEDHA_EWORKSPACE = -5, /* workspace too small */
+  MEDHA_ECUDA = -6,      /* a CUDA runtime/driver call failed (message has the CUDA error) */
+  MEDHA_ENCCL = -7       /* an NCCL call failed or the communicator is in an error state */
+};
+
+/* Human-readable name of a status code (static string). */
+const char *medha_status_str(medha_status s);
+/* Detail message of the last failing call on this thread ("" if none). */
+const char *medha_last_error(void);
+/* ABI version, (major << 16) | minor. */
+int32_t medha_version(void);
+
+/*
+ * One KVP shard of one sequence for one layer ("shards the KV cache ...
+ * along the sequence dimension").  k and v are bf16
+ * [h_kv][capacity][d] (head-major, each head's tokens contiguous).  Local token j
+ * sits at absolute position pos0 + j; tokens j >= len are never read.
+ */
+typedef struct medha_kv_shard {
+  void *k;            /* device, bf16 [h_kv][capacity][d] */
+  void *v;            /* device, bf16 [h_kv][capacity][d] */
+  int64_t capacity;   /* tokens allocated per head */
+  int64_t len;        /* tokens valid per head (0 <= len <= capacity) */
+  int64_t pos0;       /* absolute position of local token 0 */
+  int32_t h_kv;       /* KV heads */
+  int32_t d;          /* head dimension */
+} medha_kv_shard;
+
+/*
+ * kv_append (P:178-183 the KV cache grows by one row per token):
+ * copies k_new, v_new (device, bf16 [n][h_kv][d], token-major as produced by the
+ * K/V projections) into kv->k, kv->v at local tokens [len, len+n) and, on success,
+ * sets kv->len += n (host-side field).  n = 0 is a no-op.
+ * Errors: MEDHA_ERANGE if len + n > capacity; MEDHA_EINVAL for null/misaligned.
+ */
+medha_status medha_kv_append(medha_kv_shard *kv, const void *k_new, const void *v_new,
+                             int64_t n, void *stream);
+
+/*
+ * attn_decode_partial (SURVEY a3 + a5; "compute partial attention outputs
+ * based on each local KV-cache shard"): for each of `batch` sequences b, the
+ * single query q[b] (bf16 [batch][h_q][d]) at absolute position q_pos_host[b]
+ * attends over shard kvs_host[b].  Writes o (fp32 [batch][h_q][d]) and lse (fp32
+ * [batch][h_q], natural log) = the exact partial state of that shard.  The KV is
+ * split across CTAs inside the GPU and the splits are merged in a
+ * fixed order inside the same launch (run-to-run deterministic).
+ *   kvs_host, q_pos_host: host arrays of length batch (read during the call).
+ *   All shards must share h_kv and d; batch <= 4096.
+ */
+size_t medha_decode_workspace_size(int32_t batch, int32_t h_q, int32_t h_kv, int32_t d);
+medha_status medha_attn_decode_partial(const medha_kv_shard *kvs_host, int32_t batch,
+                                       const void *q, int32_t h_q, const int64_t *q_pos_host,
+                                       float scale, float *o, float *lse,
+                                       void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * attn_prefill_chunk (P:321-366 chunked prefill, Eq. 3): a chunk of c
+ * query tokens q (bf16 [c][h_q][d]) at absolute positions q_pos0 .. q_pos0+c-1
+ * attends causally over the shard `kv` (all of its len tokens that are visible).
+ * With the tail shard after medha_kv_append of the chunk's own K/V and
+ * q_pos0 = pos0 + len - c this is the chunk's full causal attention on one GPU.
+ * Writes o (fp32 [c][h_q][d]) and lse (fp32 [c][h_q]).  QK^T and PV run on the
+ * tcgen05 tensor cores with TMEM accumulators; K/V tiles are staged by TMA.
+ * c must be >= 1 and <= 65536.
+ */
+size_t medha_prefill_workspace_size(int64_t c, int32_t h_q, int32_t h_kv, int32_t d);
+medha_status medha_attn_prefill_chunk(const medha_kv_shard *kv, const void *q, int64_t c,
+                                      int32_t h_q, int64_t q_pos0, float scale,
+                                      float *o, float *lse, void *ws, size_t ws_bytes,
+                                      void *stream);
+
+/*
+ * merge_partials: parts is fp32 [P][rows*(d+1)] where part r
+ * holds o_r [rows][d] followed by lse_r [rows].  Writes o_out fp32 [rows][d],
+ * lse_out fp32 [rows] (may be NULL) and o_out_bf16 bf16 [rows][d] (may be NULL).
+ * Parts are combined in order r = 0..P-1.  1 <= P <= 64.
+ * A row whose parts are all -inf yields o = 0, lse = -inf; the call then still
+ * completes but returns nothing different (the condition is data-dependent and
+ * only visible on the device).
+ */
+medha_status medha_merge_partials(const float *parts, int32_t P, int64_t rows, int32_t d,
+                                  float *o_out, float *lse_out, void *o_out_bf16, void *stream);
+
+/*
+ * KVP communicator: an NCCL communicator over the P ranks
+ * of one KVP group, one process per GPU.  Rank 0 calls medha_kvp_unique_id and
+ * ships the 128 bytes to the other ranks out of band (the Python binding uses the
+ * torch.distributed store); every rank then calls medha_kvp_comm_create with the
+ * current CUDA device set to its GPU.
+ */
+typedef struct medha_kvp_comm medha_kvp_comm;
+medha_status medha_kvp_unique_id(uint8_t id_out[128]);
+medha_status medha_kvp_comm_create(const uint8_t id[128], int32_t rank, int32_t world,
+                                   medha_kvp_comm **out);
+medha_status medha_kvp_comm_destroy(medha_kvp_comm *comm);
+medha_status medha_kvp_comm_info(const medha_kvp_comm *comm, int32_t *rank, int32_t *world);
+
+/*
+ * kvp_decode (Eq. 5): the local partial (medha_attn_decode_partial on
+ * this rank's shards), an all-gather of the packed (o ‖ lse) partials of all
+ * ranks (rows*(d+1)*4 bytes per rank, independent of the KV length), and the
+ * rank-ordered LSE merge.  Every rank receives the identical final o_out (fp32
+ * [batch][h_q][d]), lse_out (fp32 [batch][h_q], may be NULL) and o_out_bf16 (may
+ * be NULL).  Must be called by all ranks of the communicator with the same
+ * batch/h_q/d (a collective).
+ */
+size_t medha_kvp_workspace_size(int32_t world, int32_t batch, int32_t h_q, int32_t h_kv, int32_t d);
+medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_host, int32_t batch,
+                              const void *q, int32_t h_q, const int64_t *q_pos_host, float scale,
+                              float *o_out, float *lse_out, void *o_out_bf16,
+                              void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * kvp_prefill_chunk (Eq. 6): a prefill chunk under KVP — every rank
+ * attends the replicated chunk queries over its own shard (ranks whose shard holds
+ * no visible key contribute (0, -inf)), then the partials are all-gathered and
+ * merged in rank order.  Output as medha_attn_prefill_chunk, identical on all ranks.
+ */
+size_t medha_kvp_prefill_workspace_size(int32_t world, int64_t c, int32_t h_q, int32_t h_kv, int32_t d);
+medha_status medha_kvp_prefill_chunk(medha_kvp_comm *comm, const medha_kv_shard *kv,
+                                     const void *q, int64_t c, int32_t h_q, int64_t q_pos0,
+                                     float scale, float *o_out, float *lse_out, void *o_out_bf16,
+                                     void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * decode_step_host (the end-to-end call a serving loop makes for one decode token
+ * of one sequence, batch 1): copies q_host (bf16 [h_q][d]) and, when append != 0,
+ * k_new_host / v_new_host (bf16 [h_kv][d]) host->device into the workspace,
+ * appends the new token to `kv` (kv->len += 1), runs the decode attention at
+ * position q_pos — locally when comm == NULL, otherwise as medha_kvp_decode — and
+ * copies o (fp32 [h_q][d]) and lse (fp32 [h_q]) back into o_host / lse_host.
+ * Asynchronous: the host buffers are valid after the stream is synchronised.
+ */
+size_t medha_decode_step_workspace_size(int32_t world, int32_t h_q, int32_t h_kv, int32_t d);
+medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, int32_t append,
+                                    const void *q_host, const void *k_new_host,
+                                    const void *v_new_host, int32_t h_q, int64_t q_pos,
+                                    float scale, float *o_host, float *lse_host,
+                                    void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * hbm_read_probe (measurement aid K6): streams `bytes` bytes from
+ * `src` with 16-byte loads and writes one word per CTA to `sink` (>= 4096 floats)
+ * so the reads cannot be elided.  Gives the same-run read-only HBM bandwidth.
+ */
+medha_status medha_hbm_read_probe(const void *src, size_t bytes, float *sink, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEDHA_ATTN_H_ */

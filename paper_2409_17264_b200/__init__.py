@@ -1,0 +1,314 @@
+"""Thin Python binding of libmedha_attn (C ABI in include/medha_attn.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  PyTorch supplies device memory (tensor.data_ptr()), the current
+stream and the process group used to ship the NCCL unique id.  There is no CPU
+or PyTorch fallback: if the extension is missing, importing this package
+raises.
+
+Names follow the C ABI: kv_append, attn_decode_partial,
+attn_prefill_chunk, merge_partials, kvp_decode, kvp_prefill_chunk,
+decode_step_host.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from typing import List, Optional, Sequence
+
+import torch
+
+__all__ = ["lib", "MedhaError", "KVShard", "kv_append", "attn_decode_partial", "attn_prefill_chunk",
+           "merge_partials", "KVPComm", "kvp_decode", "kvp_prefill_chunk", "decode_step_host",
+           "hbm_read_probe", "decode_workspace", "prefill_workspace", "kvp_workspace", "LIB_PATH"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmedha_attn.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libmedha_attn.so not built at {LIB_PATH}; run `python -m paper_2409_17264_b200.build` "
+                      "(there is no CPU fallback)")
+lib = ctypes.CDLL(LIB_PATH)
+
+
+class _Shard(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_void_p), ("v", ctypes.c_void_p), ("capacity", ctypes.c_int64),
+                ("len", ctypes.c_int64), ("pos0", ctypes.c_int64), ("h_kv", ctypes.c_int32),
+                ("d", ctypes.c_int32)]
+
+
+_vp, _i32, _i64, _f32, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
+_P = ctypes.POINTER
+
+
+def _sig(name, restype, *argtypes):
+    fn = getattr(lib, name)
+    fn.restype = restype
+    fn.argtypes = list(argtypes)
+    return fn
+
+
+_sig("medha_status_str", ctypes.c_char_p, _i32)
+_sig("medha_last_error", ctypes.c_char_p)
+_sig("medha_version", _i32)
+_sig("medha_kv_append", _i32, _P(_Shard), _vp, _vp, _i64, _vp)
+_sig("medha_decode_workspace_size", _sz, _i32, _i32, _i32, _i32)
+_sig("medha_attn_decode_partial", _i32, _P(_Shard), _i32, _vp, _i32, _P(_i64), _f32, _vp, _vp, _vp, _sz, _vp)
+_sig("medha_prefill_workspace_size", _sz, _i64, _i32, _i32, _i32)
+_sig("medha_attn_prefill_chunk", _i32, _P(_Shard), _vp, _i64, _i32, _i64, _f32, _vp, _vp, _vp, _sz, _vp)
+_sig("medha_merge_partials", _i32, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp)
+_sig("medha_kvp_unique_id", _i32, _vp)
+_sig("medha_kvp_comm_create", _i32, _vp, _i32, _i32, _P(_vp))
+_sig("medha_kvp_comm_destroy", _i32, _vp)
+_sig("medha_kvp_comm_info", _i32, _vp, _P(_i32), _P(_i32))
+_sig("medha_kvp_workspace_size", _sz, _i32, _i32, _i32, _i32, _i32)
+_sig("medha_kvp_decode", _i32, _vp, _P(_Shard), _i32, _vp, _i32, _P(_i64), _f32, _vp, _vp, _vp, _vp, _sz, _vp)
+_sig("medha_kvp_prefill_workspace_size", _sz, _i32, _i64, _i32, _i32, _i32)
+_sig("medha_kvp_prefill_chunk", _i32, _vp, _P(_Shard), _vp, _i64, _i32, _i64, _f32, _vp, _vp, _vp, _vp, _sz, _vp)
+_sig("medha_decode_step_workspace_size", _sz, _i32, _i32, _i32, _i32)
+_sig("medha_decode_step_host", _i32, _vp, _P(_Shard), _i32, _vp, _vp, _vp, _i32, _i64, _f32, _vp, _vp, _vp, _sz,
+     _vp)
+_sig("medha_hbm_read_probe", _i32, _vp, _sz, _vp, _vp)
+
+
+class MedhaError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        name = lib.medha_status_str(status).decode()
+        detail = lib.medha_last_error().decode()
+        super().__init__(f"{where}: {name} ({status}): {detail}")
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise MedhaError(status, where)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need_cuda(t: torch.Tensor, name: str, dtype=None):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+class KVShard:
+    """One KVP shard of one sequence: bf16 k, v [h_kv][capacity][d] on the GPU.
+
+    Local token j holds absolute position pos0 + j; `len` tokens are valid.
+    """
+
+    def __init__(self, k: torch.Tensor, v: torch.Tensor, length: int = 0, pos0: int = 0):
+        _need_cuda(k, "k", torch.bfloat16)
+        _need_cuda(v, "v", torch.bfloat16)
+        if k.shape != v.shape or k.dim() != 3:
+            raise ValueError("k, v must both be [h_kv][capacity][d]")
+        self.k, self.v = k, v
+        self.h_kv, self.capacity, self.d = k.shape
+        self.len = int(length)
+        self.pos0 = int(pos0)
+
+    @classmethod
+    def empty(cls, h_kv: int, capacity: int, d: int, pos0: int = 0, device=None):
+        k = torch.empty((h_kv, capacity, d), dtype=torch.bfloat16, device=device or "cuda")
+        v = torch.empty_like(k)
+        return cls(k, v, 0, pos0)
+
+    def c(self) -> _Shard:
+        return _Shard(self.k.data_ptr(), self.v.data_ptr(), self.capacity, self.len, self.pos0, self.h_kv, self.d)
+
+
+def _shards_c(shards: Sequence[KVShard]):
+    arr = (_Shard * len(shards))()
+    for i, s in enumerate(shards):
+        arr[i] = s.c()
+    return arr
+
+
+def _scale(scale, d):
+    return float(scale) if scale is not None else 1.0 / math.sqrt(d)
+
+
+_WS = {}
+
+
+def _workspace(kind: str, nbytes: int, device) -> torch.Tensor:
+    """Cached zero-initialised workspace (the library leaves counters zeroed)."""
+    key = (kind, torch.device(device).index)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
+def decode_workspace(batch, h_q, h_kv, d, device=None):
+    return _workspace("decode", lib.medha_decode_workspace_size(batch, h_q, h_kv, d), device or "cuda")
+
+
+def prefill_workspace(c, h_q, h_kv, d, device=None):
+    return _workspace("prefill", lib.medha_prefill_workspace_size(c, h_q, h_kv, d), device or "cuda")
+
+
+def kvp_workspace(world, batch, h_q, h_kv, d, device=None):
+    return _workspace("kvp", lib.medha_kvp_workspace_size(world, batch, h_q, h_kv, d), device or "cuda")
+
+
+def kv_append(shard: KVShard, k_new: torch.Tensor, v_new: torch.Tensor, stream=None) -> None:
+    """K1: append token-major bf16 [n][h_kv][d] rows at shard.len (shard.len += n)."""
+    _need_cuda(k_new, "k_new", torch.bfloat16)
+    _need_cuda(v_new, "v_new", torch.bfloat16)
+    n = k_new.shape[0]
+    c = shard.c()
+    _check(lib.medha_kv_append(ctypes.byref(c), _ptr(k_new), _ptr(v_new), n, _stream(stream)), "kv_append")
+    shard.len = c.len
+
+
+def attn_decode_partial(shards: Sequence[KVShard], q: torch.Tensor, q_pos: Sequence[int], scale=None,
+                        o: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
+                        ws: Optional[torch.Tensor] = None, stream=None):
+    """K3+K4: decode partial (o fp32 [B][h_q][d], lse fp32 [B][h_q]) of each sequence over its shard."""
+    _need_cuda(q, "q", torch.bfloat16)
+    B, h_q, d = q.shape
+    if len(shards) != B or len(q_pos) != B:
+        raise ValueError("need one shard and one q_pos per sequence")
+    if o is None:
+        o = torch.empty((B, h_q, d), dtype=torch.float32, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, h_q), dtype=torch.float32, device=q.device)
+    h_kv = shards[0].h_kv
+    if ws is None:
+        ws = decode_workspace(B, h_q, h_kv, d, q.device)
+    qp = (ctypes.c_int64 * B)(*[int(x) for x in q_pos])
+    _check(lib.medha_attn_decode_partial(_shards_c(shards), B, _ptr(q), h_q, qp, _scale(scale, d), _ptr(o),
+                                         _ptr(lse), _ptr(ws), ws.numel(), _stream(stream)), "attn_decode_partial")
+    return o, lse
+
+
+def attn_prefill_chunk(shard: KVShard, q: torch.Tensor, q_pos0: int, scale=None, o=None, lse=None, ws=None,
+                       stream=None):
+    """K2: chunk of c query tokens (bf16 [c][h_q][d]) at positions q_pos0.. over the shard."""
+    _need_cuda(q, "q", torch.bfloat16)
+    c, h_q, d = q.shape
+    if o is None:
+        o = torch.empty((c, h_q, d), dtype=torch.float32, device=q.device)
+    if lse is None:
+        lse = torch.empty((c, h_q), dtype=torch.float32, device=q.device)
+    if ws is None:
+        ws = prefill_workspace(c, h_q, shard.h_kv, d, q.device)
+    sh = shard.c()
+    _check(lib.medha_attn_prefill_chunk(ctypes.byref(sh), _ptr(q), c, h_q, int(q_pos0), _scale(scale, d), _ptr(o),
+                                        _ptr(lse), _ptr(ws), ws.numel(), _stream(stream)), "attn_prefill_chunk")
+    return o, lse
+
+
+def merge_partials(parts: torch.Tensor, rows: int, d: int, want_bf16: bool = False, stream=None):
+    """K5: parts fp32 [P][rows*(d+1)] (o then lse per part) -> (o [rows][d], lse [rows], o_bf16|None)."""
+    _need_cuda(parts, "parts", torch.float32)
+    P = parts.shape[0]
+    o = torch.empty((rows, d), dtype=torch.float32, device=parts.device)
+    lse = torch.empty((rows,), dtype=torch.float32, device=parts.device)
+    ob = torch.empty((rows, d), dtype=torch.bfloat16, device=parts.device) if want_bf16 else None
+    _check(lib.medha_merge_partials(_ptr(parts), P, rows, d, _ptr(o), _ptr(lse), _ptr(ob), _stream(stream)),
+           "merge_partials")
+    return o, lse, ob
+
+
+class KVPComm:
+    """NCCL communicator of one KVP group, bootstrapped over torch.distributed.
+
+    Rank 0 creates the 128-byte NCCL unique id and ships it through the
+    process group (works with gloo or nccl); every rank then creates the
+    communicator on its current CUDA device.
+    """
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        buf = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            _check(lib.medha_kvp_unique_id(buf), "kvp_unique_id")
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        _check(lib.medha_kvp_comm_create(uid, self.rank, self.world, ctypes.byref(h)), "kvp_comm_create")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _check(lib.medha_kvp_comm_destroy(self.handle), "kvp_comm_destroy")
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def kvp_decode(comm: KVPComm, shards: Sequence[KVShard], q: torch.Tensor, q_pos: Sequence[int], scale=None,
+               want_bf16=False, ws=None, stream=None):
+    """Eq. 5: local partial + NCCL all-gather + rank-ordered LSE merge; identical on all ranks."""
+    _need_cuda(q, "q", torch.bfloat16)
+    B, h_q, d = q.shape
+    o = torch.empty((B, h_q, d), dtype=torch.float32, device=q.device)
+    lse = torch.empty((B, h_q), dtype=torch.float32, device=q.device)
+    ob = torch.empty((B, h_q, d), dtype=torch.bfloat16, device=q.device) if want_bf16 else None
+    if ws is None:
+        ws = kvp_workspace(comm.world, B, h_q, shards[0].h_kv, d, q.device)
+    qp = (ctypes.c_int64 * B)(*[int(x) for x in q_pos])
+    _check(lib.medha_kvp_decode(comm.handle, _shards_c(shards), B, _ptr(q), h_q, qp, _scale(scale, d), _ptr(o),
+                                _ptr(lse), _ptr(ob), _ptr(ws), ws.numel(), _stream(stream)), "kvp_decode")
+    return o, lse, ob
+
+
+def kvp_prefill_chunk(comm: KVPComm, shard: KVShard, q: torch.Tensor, q_pos0: int, scale=None, want_bf16=False,
+                      ws=None, stream=None):
+    """Eq. 6: prefill chunk under KVP (each rank over its shard, then all-gather + merge)."""
+    _need_cuda(q, "q", torch.bfloat16)
+    c, h_q, d = q.shape
+    o = torch.empty((c, h_q, d), dtype=torch.float32, device=q.device)
+    lse = torch.empty((c, h_q), dtype=torch.float32, device=q.device)
+    ob = torch.empty((c, h_q, d), dtype=torch.bfloat16, device=q.device) if want_bf16 else None
+    if ws is None:
+        ws = _workspace("kvp_prefill", lib.medha_kvp_prefill_workspace_size(comm.world, c, h_q, shard.h_kv, d),
+                        q.device)
+    sh = shard.c()
+    _check(lib.medha_kvp_prefill_chunk(comm.handle, ctypes.byref(sh), _ptr(q), c, h_q, int(q_pos0), _scale(scale, d),
+                                       _ptr(o), _ptr(lse), _ptr(ob), _ptr(ws), ws.numel(), _stream(stream)),
+           "kvp_prefill_chunk")
+    return o, lse, ob
+
+
+def decode_step_host(comm: Optional[KVPComm], shard: KVShard, append: bool, q_host: torch.Tensor,
+                     k_host: Optional[torch.Tensor], v_host: Optional[torch.Tensor], q_pos: int,
+                     o_host: torch.Tensor, lse_host: Optional[torch.Tensor], ws: torch.Tensor, scale=None,
+                     stream=None) -> None:
+    """End-to-end decode step with host (pinned) buffers; async on the stream."""
+    h_q, d = q_host.shape
+    sh = shard.c()
+    _check(lib.medha_decode_step_host(comm.handle if comm is not None else None, ctypes.byref(sh), int(bool(append)),
+                                      _ptr(q_host), _ptr(k_host), _ptr(v_host), h_q, int(q_pos), _scale(scale, d),
+                                      _ptr(o_host), _ptr(lse_host), _ptr(ws), ws.numel(), _stream(stream)),
+           "decode_step_host")
+    shard.len = sh.len
+
+
+def decode_step_workspace(world, h_q, h_kv, d, device=None):
+    return _workspace(f"step{world}", lib.medha_decode_step_workspace_size(world, h_q, h_kv, d), device or "cuda")
+
+
+def hbm_read_probe(src: torch.Tensor, sink: torch.Tensor, stream=None) -> None:
+    _check(lib.medha_hbm_read_probe(_ptr(src), src.numel() * src.element_size(), _ptr(sink), _stream(stream)),
+           "hbm_read_probe")

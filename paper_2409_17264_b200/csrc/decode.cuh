@@ -1,0 +1,313 @@
+// decode.cuh — K3 split-KV decode partial with the K4 split merge fused into the
+// last CTA of every (sequence, kv head).  SURVEY.md §8(a) a3 + a5.
+//
+// P:178-183 "During decode, we scan the entire KV cache so far" — the kernel is
+// bound by HBM: every K/V byte of the visible shard is read exactly once (GQA
+// packing: the G query heads of one KV head share each loaded byte),
+// and the KV range is split across CTAs inside the GPU.
+//
+// Data path per warp and 16-token tile (D = 128):
+//   * K rows: lane (g = lane/4, c = lane%4) loads tokens g and 8+g, bytes
+//     [64i + 16c, +16) for i < D/32 -> every LDG.128 of the warp covers 8 full
+//     64-byte row segments (coalesced), 2 KiB of K per warp instruction group.
+//   * V rows: lane (g, c) loads tokens 2c, 2c+1, 2c+8, 2c+9, bytes [16g, +16) and
+//     [128 + 16g, +16) -> 8 lanes read one 128-byte row segment.
+//   * S = Q.K^T and O += P.V are legacy warp MMAs (m16n8k16, bf16 in, fp32 out)
+//     used as dot-product engines: the FFMA pipe could not keep up with HBM at
+//     G = 8.  The head dimension is permuted identically for Q and K
+//     (any permutation leaves q.k unchanged), which is what lets each lane use
+//     its own 16-byte loads directly as B fragments; V fragments are built with
+//     PRMT.  Query heads sit on the MMA M dimension (rows g and g+8).
+//   * fp32 online softmax in base 2 (scale*log2e folded into one multiply);
+//     P rounded to bf16 (RNE) before the PV MMA (reading R8).
+// Per-CTA: 4 warps interleave 16-token tiles; their (m, l, O) are merged through
+// shared memory; the CTA writes a normalised (o, lse2) split partial; the last
+// CTA of a (seq, kv head) (atomic ticket) merges all splits in split order.
+#pragma once
+#include "common.cuh"
+
+namespace medha {
+
+constexpr int kDecodeMaxSeqPerLaunch = 64;
+constexpr int kDecodeWarps = 4;
+constexpr int kDecodeThreads = kDecodeWarps * 32;
+
+struct DecodeSeq {
+  const __nv_bfloat16 *k;  // [h_kv][cap][D]
+  const __nv_bfloat16 *v;
+  int64_t cap;
+  int64_t n_vis;         // visible local tokens (keys 0..n_vis-1)
+  int32_t split_tokens;  // tokens per split, multiple of 64
+  int32_t n_splits;      // splits per kv head
+  int32_t cta_begin;     // first CTA of this sequence (CTAs ordered [kvh][split])
+  int32_t slot_begin;    // first workspace slot of this sequence
+};
+
+struct DecodeParams {
+  const __nv_bfloat16 *q;  // [batch][h_q][D] (this launch's first sequence at q)
+  float *o;                // [batch][h_q][D]
+  float *lse;              // [batch][h_q], natural log
+  float *ws_o;             // [slot][G][D] normalised split outputs
+  float *ws_lse;           // [slot][G] base-2 split lse
+  unsigned *counters;      // [n_seq * h_kv]
+  float scale_log2;        // softmax scale * log2(e)
+  int32_t n_seq;
+  int32_t h_kv;
+  int32_t h_q;
+  DecodeSeq seq[kDecodeMaxSeqPerLaunch];
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const __grid_constant__ DecodeParams p) {
+  static_assert(D == 64 || D == 128, "D");
+  static_assert(G >= 1 && G <= 16, "G");
+  constexpr int KCH = D / 32;   // 16-byte K chunks per lane per token
+  constexpr int VCH = D / 64;   // 16-byte V chunks per lane per token
+  constexpr int KS = D / 16;    // k-steps of the QK MMA
+  constexpr int NT = D / 8;     // n-tiles of the PV MMA
+  constexpr bool kHi = (G > 8); // rows g+8 carry heads 8..15
+
+  __shared__ float sm_o[kDecodeWarps][G][D];
+  __shared__ float sm_m[kDecodeWarps][G];
+  __shared__ float sm_l[kDecodeWarps][G];
+  __shared__ unsigned sm_ticket;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int g = lane >> 2;
+  const int c = lane & 3;
+
+  // ---- which (sequence, kv head, split) is this CTA -------------------------------
+  int sidx = 0;
+  while (sidx + 1 < p.n_seq && (int)blockIdx.x >= p.seq[sidx + 1].cta_begin) ++sidx;
+  const DecodeSeq &S = p.seq[sidx];
+  const int local = (int)blockIdx.x - S.cta_begin;
+  const int kvh = local / S.n_splits;
+  const int split = local - kvh * S.n_splits;
+  const int64_t t_begin = (int64_t)split * S.split_tokens;
+  const int64_t t_end = min64(t_begin + S.split_tokens, S.n_vis);
+
+  const __nv_bfloat16 *kbase = S.k + (int64_t)kvh * S.cap * D;
+  const __nv_bfloat16 *vbase = S.v + (int64_t)kvh * S.cap * D;
+
+  // ---- Q fragments (rows g / g+8 = heads of this group), permuted like K ------------
+  uint32_t qlo[KS][2], qhi[KS][2];
+  {
+    const __nv_bfloat16 *qrow = p.q + ((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D;
+#pragma unroll
+    for (int i = 0; i < KCH; ++i) {
+      uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+      if (g < G) a = *reinterpret_cast<const uint4 *>(qrow + (int64_t)g * D + 32 * i + 8 * c);
+      if (kHi && g + 8 < G) b = *reinterpret_cast<const uint4 *>(qrow + (int64_t)(g + 8) * D + 32 * i + 8 * c);
+      qlo[2 * i][0] = a.x; qlo[2 * i][1] = a.y; qlo[2 * i + 1][0] = a.z; qlo[2 * i + 1][1] = a.w;
+      qhi[2 * i][0] = b.x; qhi[2 * i][1] = b.y; qhi[2 * i + 1][0] = b.z; qhi[2 * i + 1][1] = b.w;
+    }
+  }
+
+  float oacc[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+  float m_lo = -INFINITY, m_hi = -INFINITY;  // running max (base 2) of rows g, g+8
+  float l_lo = 0.f, l_hi = 0.f;              // thread-partial running sums
+
+  uint4 kr[2][KCH], vr[4][VCH];
+  auto load_tile = [&](int64_t tb, uint4 (&kk)[2][KCH], uint4 (&vv)[4][VCH]) {
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      const int64_t tok = tb + 8 * n + g;
+      const bool ok = tok < t_end;
+      const __nv_bfloat16 *src = kbase + tok * D + 8 * c;
+#pragma unroll
+      for (int i = 0; i < KCH; ++i) kk[n][i] = ok ? ldg_stream(src + 32 * i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t tok = tb + 2 * c + (r & 1) + 8 * (r >> 1);
+      const bool ok = tok < t_end;
+      const __nv_bfloat16 *src = vbase + tok * D + 8 * g;
+#pragma unroll
+      for (int i = 0; i < VCH; ++i) vv[r][i] = ok ? ldg_stream(src + 64 * i) : make_uint4(0, 0, 0, 0);
+    }
+  };
+
+  int64_t tb = t_begin + 16 * warp;
+  if (tb < t_end) load_tile(tb, kr, vr);
+  for (; tb < t_end; tb += 16 * kDecodeWarps) {
+    uint4 kn[2][KCH], vn[4][VCH];
+    const int64_t nb = tb + 16 * kDecodeWarps;
+    if (nb < t_end) load_tile(nb, kn, vn);
+
+    // ---- S = Q K^T  (rows: heads g / g+8; cols: tokens 2c,2c+1 of n-tile n) ----------
+    float s[2][4];
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const uint4 &kv4 = kr[n][ks >> 1];
+        const uint32_t b0 = (ks & 1) ? kv4.z : kv4.x;
+        const uint32_t b1 = (ks & 1) ? kv4.w : kv4.y;
+        mma_bf16_16816(s[n], qlo[ks][0], qhi[ks][0], qlo[ks][1], qhi[ks][1], b0, b1);
+      }
+    }
+    // ---- masking + online softmax (base 2) ------------------------------------------
+    float mx_lo = -INFINITY, mx_hi = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool ok = (tb + 8 * n + 2 * c + e) < t_end;
+        s[n][e] = ok ? s[n][e] * p.scale_log2 : -INFINITY;
+        s[n][2 + e] = ok ? s[n][2 + e] * p.scale_log2 : -INFINITY;
+        mx_lo = fmaxf(mx_lo, s[n][e]);
+        mx_hi = fmaxf(mx_hi, s[n][2 + e]);
+      }
+    }
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
+    if (kHi) {
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
+    }
+    const float mn_lo = fmaxf(m_lo, mx_lo);
+    const float mu_lo = (mn_lo == -INFINITY) ? 0.f : mn_lo;
+    const float al_lo = fast_exp2(m_lo - mu_lo);  // m_lo = -inf -> 0
+    m_lo = mn_lo;
+    float mu_hi = 0.f, al_hi = 1.f;
+    if (kHi) {
+      const float mn_hi = fmaxf(m_hi, mx_hi);
+      mu_hi = (mn_hi == -INFINITY) ? 0.f : mn_hi;
+      al_hi = fast_exp2(m_hi - mu_hi);
+      m_hi = mn_hi;
+    }
+    float pr[2][4];
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      pr[n][0] = fast_exp2(s[n][0] - mu_lo);
+      pr[n][1] = fast_exp2(s[n][1] - mu_lo);
+      pr[n][2] = kHi ? fast_exp2(s[n][2] - mu_hi) : 0.f;
+      pr[n][3] = kHi ? fast_exp2(s[n][3] - mu_hi) : 0.f;
+    }
+    l_lo = l_lo * al_lo + (pr[0][0] + pr[0][1] + pr[1][0] + pr[1][1]);
+    if (kHi) l_hi = l_hi * al_hi + (pr[0][2] + pr[0][3] + pr[1][2] + pr[1][3]);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      oacc[j][0] *= al_lo;
+      oacc[j][1] *= al_lo;
+      if (kHi) {
+        oacc[j][2] *= al_hi;
+        oacc[j][3] *= al_hi;
+      }
+    }
+    // ---- O += P V --------------------------------------------------------------------
+    const uint32_t a0 = pack_bf16x2(pr[0][0], pr[0][1]);
+    const uint32_t a1 = kHi ? pack_bf16x2(pr[0][2], pr[0][3]) : 0u;
+    const uint32_t a2 = pack_bf16x2(pr[1][0], pr[1][1]);
+    const uint32_t a3 = kHi ? pack_bf16x2(pr[1][2], pr[1][3]) : 0u;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int ch = j >> 3, e = j & 7;
+      const uint32_t sel = (e & 1) ? 0x7632u : 0x5410u;
+      const uint32_t *r0 = reinterpret_cast<const uint32_t *>(&vr[0][ch]);
+      const uint32_t *r1 = reinterpret_cast<const uint32_t *>(&vr[1][ch]);
+      const uint32_t *r2 = reinterpret_cast<const uint32_t *>(&vr[2][ch]);
+      const uint32_t *r3 = reinterpret_cast<const uint32_t *>(&vr[3][ch]);
+      const uint32_t b0 = prmt(r0[e >> 1], r1[e >> 1], sel);
+      const uint32_t b1 = prmt(r2[e >> 1], r3[e >> 1], sel);
+      mma_bf16_16816(oacc[j], a0, a1, a2, a3, b0, b1);
+    }
+    if (nb < t_end) {
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int i = 0; i < KCH; ++i) kr[n][i] = kn[n][i];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int i = 0; i < VCH; ++i) vr[r][i] = vn[r][i];
+    }
+  }
+
+  // ---- per-warp reduction of l over the 4 lanes of a row, publish to smem --------------
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
+  if (kHi) {
+    l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
+    l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
+  }
+  if (c == 0) {
+    if (g < G) { sm_m[warp][g] = m_lo; sm_l[warp][g] = l_lo; }
+    if (kHi && g + 8 < G) { sm_m[warp][g + 8] = m_hi; sm_l[warp][g + 8] = l_hi; }
+  }
+  // O fragment n-tile j, element e in {0,1}: head row g (+8), d = 64*(j/8) + 8*(2c+e) + (j%8)
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int dd = 64 * (j >> 3) + 8 * (2 * c + e) + (j & 7);
+      if (g < G) sm_o[warp][g][dd] = oacc[j][e];
+      if (kHi && g + 8 < G) sm_o[warp][g + 8][dd] = oacc[j][2 + e];
+    }
+  }
+  __syncthreads();
+
+  // ---- CTA merge of the 4 warps: (o normalised, lse2) of this split ---------------------
+  const bool single = (S.n_splits == 1);
+  const int64_t slot = (int64_t)S.slot_begin + (int64_t)kvh * S.n_splits + split;
+  float *dst_o = single ? (p.o + ((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D) : (p.ws_o + slot * G * D);
+  for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
+    const int row = idx / D, dd = idx - row * D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kDecodeWarps; ++w) M = fmaxf(M, sm_m[w][row]);
+    float L = 0.f, acc = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kDecodeWarps; ++w) {
+        const float sc = fast_exp2(sm_m[w][row] - M);
+        L += sm_l[w][row] * sc;
+        acc += sm_o[w][row][dd] * sc;
+      }
+    }
+    dst_o[idx] = (L > 0.f) ? acc / L : 0.f;
+    if (dd == 0) {
+      const float lse2 = (L > 0.f) ? M + __log2f(L) : -INFINITY;
+      if (single)
+        p.lse[(int64_t)sidx * p.h_q + (int64_t)kvh * G + row] = lse2 * kLn2;
+      else
+        p.ws_lse[slot * G + row] = lse2;
+    }
+  }
+  if (single) return;
+
+  // ---- last CTA of this (seq, kv head) merges the splits in split order -----------------
+  __threadfence();
+  __syncthreads();
+  unsigned *ctr = p.counters + (int64_t)sidx * p.h_kv + kvh;
+  if (tid == 0) sm_ticket = atomicAdd(ctr, 1u);
+  __syncthreads();
+  if (sm_ticket != (unsigned)(S.n_splits - 1)) return;
+  __threadfence();
+  const int64_t slot0 = (int64_t)S.slot_begin + (int64_t)kvh * S.n_splits;
+  const int ns = S.n_splits;
+  for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
+    const int row = idx / D, dd = idx - row * D;
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < ns; ++s2) M = fmaxf(M, __ldcg(p.ws_lse + (slot0 + s2) * G + row));
+    float L = 0.f, acc = 0.f;
+    if (M != -INFINITY) {
+      for (int s2 = 0; s2 < ns; ++s2) {
+        const float sc = fast_exp2(__ldcg(p.ws_lse + (slot0 + s2) * G + row) - M);
+        L += sc;
+        acc += sc * __ldcg(p.ws_o + (slot0 + s2) * G * D + idx);
+      }
+    }
+    const int64_t orow = (int64_t)sidx * p.h_q + (int64_t)kvh * G + row;
+    p.o[orow * D + dd] = (L > 0.f) ? acc / L : 0.f;
+    if (dd == 0) p.lse[orow] = (L > 0.f) ? (M + __log2f(L)) * kLn2 : -INFINITY;
+  }
+  if (tid == 0) *ctr = 0u;  // leave the counter zeroed for the next call
+}
+
+}  // namespace medha

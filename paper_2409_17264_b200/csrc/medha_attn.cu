@@ -1,0 +1,629 @@
+// medha_attn.cu — host side of libmedha_attn (C ABI declared in include/medha_attn.h).
+// Validation, work planning (split-KV sizing to the SM count), TMA descriptor
+// encoding, NCCL KVP communicator and the all-gather + merge orchestration.
+// Every compute step runs in the kernels of decode.cuh / prefill_tc.cuh / misc.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "medha_attn.h"
+#include "decode.cuh"
+#include "misc.cuh"
+#include "prefill_tc.cuh"
+
+using namespace medha;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+medha_status fail(medha_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess) return fail(MEDHA_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_));   \
+  } while (0)
+
+#define LAUNCH_CHECK(what)                                                                      \
+  do {                                                                                          \
+    cudaError_t e_ = cudaGetLastError();                                                        \
+    if (e_ != cudaSuccess) return fail(MEDHA_ECUDA, "%s launch: %s", what, cudaGetErrorString(e_)); \
+  } while (0)
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+bool supported_g(int G) { return G == 1 || G == 2 || G == 4 || G == 8 || G == 16; }
+bool supported_d(int d) { return d == 64 || d == 128; }
+
+medha_status check_shard(const medha_kv_shard *kv) {
+  if (!kv) return fail(MEDHA_EINVAL, "null shard");
+  if (!kv->k || !kv->v) return fail(MEDHA_EINVAL, "null shard k/v pointer");
+  if (!aligned16(kv->k) || !aligned16(kv->v)) return fail(MEDHA_EINVAL, "shard k/v not 16-byte aligned");
+  if (kv->h_kv <= 0 || kv->capacity < 0 || kv->len < 0) return fail(MEDHA_EINVAL, "bad shard sizes");
+  if (kv->len > kv->capacity) return fail(MEDHA_ERANGE, "shard len %lld > capacity %lld", (long long)kv->len,
+                                          (long long)kv->capacity);
+  if (!supported_d(kv->d)) return fail(MEDHA_ENOTSUP, "head dim %d not in {64,128}", kv->d);
+  return MEDHA_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// decode
+// ---------------------------------------------------------------------------------------------
+constexpr int kDecodeCtaBudget = 1024;  // upper bound of split CTAs per launch (workspace sizing)
+
+struct DecodeWs {
+  unsigned *counters;
+  float *ws_lse;
+  float *ws_o;
+  size_t bytes;
+};
+
+size_t decode_ws_layout(int32_t batch, int32_t h_q, int32_t h_kv, int32_t d, char *base, DecodeWs *out) {
+  const int64_t nb = std::min<int64_t>(std::max<int32_t>(batch, 1), kDecodeMaxSeqPerLaunch);
+  const int64_t G = h_kv > 0 ? h_q / h_kv : 1;
+  const int64_t slots = kDecodeCtaBudget + nb * h_kv;
+  size_t off = 0;
+  const size_t c_off = off;
+  off = round_up(off + nb * h_kv * sizeof(unsigned), 256);
+  const size_t l_off = off;
+  off = round_up(off + slots * G * sizeof(float), 256);
+  const size_t o_off = off;
+  off = round_up(off + slots * G * d * sizeof(float), 256);
+  if (out) {
+    out->counters = reinterpret_cast<unsigned *>(base + c_off);
+    out->ws_lse = reinterpret_cast<float *>(base + l_off);
+    out->ws_o = reinterpret_cast<float *>(base + o_off);
+    out->bytes = off;
+  }
+  return off;
+}
+
+template <int D, int G>
+void launch_decode(const DecodeParams &p, int grid, cudaStream_t st) {
+  decode_splitkv_kernel<D, G><<<grid, kDecodeThreads, 0, st>>>(p);
+}
+
+template <int D>
+medha_status dispatch_decode_g(int G, const DecodeParams &p, int grid, cudaStream_t st) {
+  switch (G) {
+    case 1: launch_decode<D, 1>(p, grid, st); break;
+    case 2: launch_decode<D, 2>(p, grid, st); break;
+    case 4: launch_decode<D, 4>(p, grid, st); break;
+    case 8: launch_decode<D, 8>(p, grid, st); break;
+    case 16: launch_decode<D, 16>(p, grid, st); break;
+    default: return fail(MEDHA_ENOTSUP, "group size %d", G);
+  }
+  LAUNCH_CHECK("decode_splitkv_kernel");
+  return MEDHA_OK;
+}
+
+medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const void *q, int32_t h_q,
+                                 const int64_t *q_pos, float scale, float *o, float *lse, void *ws,
+                                 size_t ws_bytes, cudaStream_t st) {
+  if (batch < 0) return fail(MEDHA_EINVAL, "negative batch");
+  if (batch == 0) return MEDHA_OK;
+  if (!kvs || !q || !q_pos || !o || !lse) return fail(MEDHA_EINVAL, "null argument");
+  if (batch > 4096) return fail(MEDHA_ENOTSUP, "batch %d > 4096", batch);
+  if (!aligned16(q)) return fail(MEDHA_EINVAL, "q not 16-byte aligned");
+  if (!(scale > 0.f)) return fail(MEDHA_EINVAL, "scale must be > 0");
+  const int32_t h_kv = kvs[0].h_kv, d = kvs[0].d;
+  for (int b = 0; b < batch; ++b) {
+    medha_status s = check_shard(&kvs[b]);
+    if (s) return s;
+    if (kvs[b].h_kv != h_kv || kvs[b].d != d) return fail(MEDHA_ESHAPE, "shards disagree on h_kv/d");
+  }
+  if (h_q <= 0 || h_q % h_kv != 0) return fail(MEDHA_EINVAL, "h_q %d not a multiple of h_kv %d", h_q, h_kv);
+  const int G = h_q / h_kv;
+  if (!supported_g(G)) return fail(MEDHA_ENOTSUP, "group size %d not in {1,2,4,8,16}", G);
+  DecodeWs W;
+  if (!ws) return fail(MEDHA_EWORKSPACE, "null workspace");
+  decode_ws_layout(batch, h_q, h_kv, d, static_cast<char *>(ws), &W);
+  if (ws_bytes < W.bytes) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, W.bytes);
+
+  const int target = 2 * num_sms();  // two 4-warp CTAs per SM
+  for (int b0 = 0; b0 < batch; b0 += kDecodeMaxSeqPerLaunch) {
+    const int nb = std::min(kDecodeMaxSeqPerLaunch, batch - b0);
+    DecodeParams p;
+    memset(&p, 0, sizeof(p));
+    p.q = static_cast<const __nv_bfloat16 *>(q) + (int64_t)b0 * h_q * d;
+    p.o = o + (int64_t)b0 * h_q * d;
+    p.lse = lse + (int64_t)b0 * h_q;
+    p.ws_o = W.ws_o;
+    p.ws_lse = W.ws_lse;
+    p.counters = W.counters;
+    p.scale_log2 = scale * kLog2e;
+    p.n_seq = nb;
+    p.h_kv = h_kv;
+    p.h_q = h_q;
+    int64_t total = 0;
+    std::vector<int64_t> nvis(nb);
+    for (int i = 0; i < nb; ++i) {
+      const medha_kv_shard &kv = kvs[b0 + i];
+      nvis[i] = std::max<int64_t>(0, std::min<int64_t>(kv.len, q_pos[b0 + i] - kv.pos0 + 1));
+      total += nvis[i] * h_kv;
+    }
+    const int64_t per_cta = std::max<int64_t>(256, round_up((size_t)cdiv(std::max<int64_t>(total, 1), target), 64));
+    int cta = 0;
+    for (int i = 0; i < nb; ++i) {
+      const medha_kv_shard &kv = kvs[b0 + i];
+      int64_t ns = std::max<int64_t>(1, cdiv(nvis[i], per_cta));
+      int64_t split_tokens = std::max<int64_t>(64, (int64_t)round_up((size_t)cdiv(std::max<int64_t>(nvis[i], 1), ns), 64));
+      ns = std::max<int64_t>(1, cdiv(nvis[i], split_tokens));
+      if (split_tokens > INT32_MAX) return fail(MEDHA_ERANGE, "split too large");
+      DecodeSeq &S = p.seq[i];
+      S.k = static_cast<const __nv_bfloat16 *>(kv.k);
+      S.v = static_cast<const __nv_bfloat16 *>(kv.v);
+      S.cap = kv.capacity;
+      S.n_vis = nvis[i];
+      S.split_tokens = (int32_t)split_tokens;
+      S.n_splits = (int32_t)ns;
+      S.cta_begin = cta;
+      S.slot_begin = cta;
+      cta += (int)(ns * h_kv);
+    }
+    if (cta > kDecodeCtaBudget + nb * h_kv) return fail(MEDHA_EWORKSPACE, "split plan exceeds workspace");
+    medha_status s = (d == 128) ? dispatch_decode_g<128>(G, p, cta, st) : dispatch_decode_g<64>(G, p, cta, st);
+    if (s) return s;
+  }
+  return MEDHA_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// prefill
+// ---------------------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                      const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t get_encode_tiled() {
+  static PFN_encodeTiled_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(ptr);
+  });
+  return fn;
+}
+
+medha_status make_map_3d(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
+                         uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2) {
+  PFN_encodeTiled_t enc = get_encode_tiled();
+  if (!enc) return fail(MEDHA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1_bytes, s2_bytes};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MEDHA_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return MEDHA_OK;
+}
+
+struct PrefillPlan {
+  int m_tiles, n_split, tiles_per_split;
+  int64_t rows, part_stride;
+  size_t ws_bytes;
+};
+
+PrefillPlan plan_prefill(int64_t c, int32_t h_q, int32_t h_kv, int32_t d, int64_t n_kv_max) {
+  PrefillPlan pl;
+  const int G = h_kv > 0 ? std::max(1, h_q / h_kv) : 1;
+  const int TQ = kTileM / std::max(1, std::min(G, kTileM));
+  pl.m_tiles = (int)cdiv(std::max<int64_t>(c, 1), TQ);
+  pl.rows = c * h_q;
+  pl.part_stride = (int64_t)round_up((size_t)(pl.rows * (d + 1)), 4);
+  const int64_t kv_tiles = std::max<int64_t>(1, cdiv(n_kv_max, kTileN));
+  const int64_t base_ctas = (int64_t)pl.m_tiles * h_kv;
+  const int sms = num_sms();
+  int ns = 1;
+  if (base_ctas < sms) {
+    // split the KV range until the grid fills the GPU, keeping >= 4 KV tiles per split
+    ns = (int)std::min<int64_t>(cdiv(sms, base_ctas), std::max<int64_t>(1, kv_tiles / 4));
+    ns = std::max(1, std::min(ns, 64));
+  }
+  pl.tiles_per_split = (int)cdiv(kv_tiles, ns);
+  pl.n_split = (int)cdiv(kv_tiles, pl.tiles_per_split);
+  pl.ws_bytes = pl.n_split > 1 ? (size_t)pl.n_split * pl.part_stride * sizeof(float) : 0;
+  return pl;
+}
+
+size_t prefill_ws_bound(int64_t c, int32_t h_q, int32_t d) {
+  const int64_t rows = c * h_q;
+  return (size_t)64 * round_up((size_t)(rows * (d + 1)), 4) * sizeof(float) + 256;
+}
+
+template <int D, int G>
+medha_status launch_prefill(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv,
+                            const PrefillParams &p, dim3 grid, cudaStream_t st) {
+  using L = PrefillLayout<D>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    CUDA_TRY(cudaFuncSetAttribute(prefill_tc_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kAlloc));
+    attr_done = true;
+  }
+  prefill_tc_kernel<D, G><<<grid, kPrefillThreads, L::kAlloc, st>>>(mq, mk, mv, p);
+  LAUNCH_CHECK("prefill_tc_kernel");
+  return MEDHA_OK;
+}
+
+template <int D>
+medha_status dispatch_prefill_g(int G, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv,
+                                const PrefillParams &p, dim3 grid, cudaStream_t st) {
+  switch (G) {
+    case 1: return launch_prefill<D, 1>(mq, mk, mv, p, grid, st);
+    case 2: return launch_prefill<D, 2>(mq, mk, mv, p, grid, st);
+    case 4: return launch_prefill<D, 4>(mq, mk, mv, p, grid, st);
+    case 8: return launch_prefill<D, 8>(mq, mk, mv, p, grid, st);
+    case 16: return launch_prefill<D, 16>(mq, mk, mv, p, grid, st);
+    default: return fail(MEDHA_ENOTSUP, "group size %d", G);
+  }
+}
+
+medha_status merge_impl(const float *parts, int32_t P, int64_t rows, int64_t part_stride, int32_t d, float *o_out,
+                        float *lse_out, void *o_bf16, cudaStream_t st) {
+  if (rows == 0) return MEDHA_OK;
+  const int warps_per_block = 8;
+  const int64_t blocks = cdiv(rows, warps_per_block);
+  if (blocks > INT32_MAX) return fail(MEDHA_ERANGE, "too many rows");
+  if (d == 128)
+    lse_merge_kernel<128><<<(unsigned)blocks, 32 * warps_per_block, 0, st>>>(parts, P, rows, part_stride, o_out, lse_out,
+                                                                            static_cast<__nv_bfloat16 *>(o_bf16));
+  else
+    lse_merge_kernel<64><<<(unsigned)blocks, 32 * warps_per_block, 0, st>>>(parts, P, rows, part_stride, o_out, lse_out,
+                                                                           static_cast<__nv_bfloat16 *>(o_bf16));
+  LAUNCH_CHECK("lse_merge_kernel");
+  return MEDHA_OK;
+}
+
+medha_status prefill_impl(const medha_kv_shard *kv, const void *q, int64_t c, int32_t h_q, int64_t q_pos0,
+                          float scale, float *o, float *lse, void *ws, size_t ws_bytes, cudaStream_t st) {
+  medha_status s = check_shard(kv);
+  if (s) return s;
+  if (c < 0) return fail(MEDHA_EINVAL, "negative chunk");
+  if (c == 0) return MEDHA_OK;
+  if (c > 65536) return fail(MEDHA_ENOTSUP, "chunk %lld > 65536", (long long)c);
+  if (!q || !o || !lse) return fail(MEDHA_EINVAL, "null argument");
+  if (!aligned16(q) || !aligned16(o)) return fail(MEDHA_EINVAL, "q/o not 16-byte aligned");
+  if (!(scale > 0.f)) return fail(MEDHA_EINVAL, "scale must be > 0");
+  const int32_t h_kv = kv->h_kv, d = kv->d;
+  if (h_q <= 0 || h_q % h_kv != 0) return fail(MEDHA_EINVAL, "h_q %d not a multiple of h_kv %d", h_q, h_kv);
+  const int G = h_q / h_kv;
+  if (!supported_g(G)) return fail(MEDHA_ENOTSUP, "group size %d not in {1,2,4,8,16}", G);
+  if (kv->capacity > INT32_MAX) return fail(MEDHA_ENOTSUP, "capacity > 2^31 tokens");
+  const int64_t n_kv_max = std::max<int64_t>(0, std::min<int64_t>(kv->len, q_pos0 + c - 1 - kv->pos0 + 1));
+  PrefillPlan pl = plan_prefill(c, h_q, h_kv, d, n_kv_max);
+  if (pl.n_split > 1) {
+    if (!ws || !aligned16(ws)) return fail(MEDHA_EWORKSPACE, "null/misaligned workspace");
+    if (ws_bytes < pl.ws_bytes) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, pl.ws_bytes);
+  }
+  CUtensorMap mq, mk, mv;
+  const int TQ = kTileM / G;
+  if ((s = make_map_3d(&mq, q, d, h_q, c, (uint64_t)d * 2, (uint64_t)h_q * d * 2, 64, G, TQ))) return s;
+  const uint64_t len_ext = (uint64_t)std::max<int64_t>(kv->len, 1);
+  if ((s = make_map_3d(&mk, kv->k, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64, kTileN, 1)))
+    return s;
+  if ((s = make_map_3d(&mv, kv->v, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64, kTileN, 1)))
+    return s;
+  PrefillParams p;
+  memset(&p, 0, sizeof(p));
+  p.o = pl.n_split > 1 ? static_cast<float *>(ws) : o;
+  p.lse = lse;
+  p.c = c;
+  p.len = kv->len;
+  p.pos0 = kv->pos0;
+  p.q_pos0 = q_pos0;
+  p.rows = pl.rows;
+  p.part_stride = pl.part_stride;
+  p.h_q = h_q;
+  p.h_kv = h_kv;
+  p.n_split = pl.n_split;
+  p.tiles_per_split = pl.tiles_per_split;
+  p.scale_log2 = scale * kLog2e;
+  dim3 grid(pl.m_tiles, h_kv, pl.n_split);
+  s = (d == 128) ? dispatch_prefill_g<128>(G, mq, mk, mv, p, grid, st) : dispatch_prefill_g<64>(G, mq, mk, mv, p, grid, st);
+  if (s) return s;
+  if (pl.n_split > 1) return merge_impl(static_cast<float *>(ws), pl.n_split, pl.rows, pl.part_stride, d, o, lse, nullptr, st);
+  return MEDHA_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+struct medha_kvp_comm {
+  ncclComm_t nccl;
+  int32_t rank, world;
+};
+
+extern "C" {
+
+const char *medha_status_str(medha_status s) {
+  switch (s) {
+    case MEDHA_OK: return "MEDHA_OK";
+    case MEDHA_EINVAL: return "MEDHA_EINVAL";
+    case MEDHA_ESHAPE: return "MEDHA_ESHAPE";
+    case MEDHA_ERANGE: return "MEDHA_ERANGE";
+    case MEDHA_ENOTSUP: return "MEDHA_ENOTSUP";
+    case MEDHA_EWORKSPACE: return "MEDHA_EWORKSPACE";
+    case MEDHA_ECUDA: return "MEDHA_ECUDA";
+    case MEDHA_ENCCL: return "MEDHA_ENCCL";
+    default: return "MEDHA_UNKNOWN";
+  }
+}
+
+const char *medha_last_error(void) { return g_last_error.c_str(); }
+
+int32_t medha_version(void) { return (1 << 16) | 0; }
+
+medha_status medha_kv_append(medha_kv_shard *kv, const void *k_new, const void *v_new, int64_t n, void *stream) {
+  medha_status s = check_shard(kv);
+  if (s) return s;
+  if (n < 0) return fail(MEDHA_EINVAL, "negative n");
+  if (n == 0) return MEDHA_OK;
+  if (!k_new || !v_new) return fail(MEDHA_EINVAL, "null k_new/v_new");
+  if (!aligned16(k_new) || !aligned16(v_new)) return fail(MEDHA_EINVAL, "k_new/v_new not 16-byte aligned");
+  if (kv->len + n > kv->capacity)
+    return fail(MEDHA_ERANGE, "append %lld tokens at len %lld exceeds capacity %lld", (long long)n, (long long)kv->len,
+                (long long)kv->capacity);
+  const int32_t vec = kv->d / 8;
+  const int64_t total = n * kv->h_kv * vec;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>(cdiv(total, threads), (int64_t)num_sms() * 8);
+  kv_append_kernel<<<(unsigned)blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4 *>(k_new), static_cast<const uint4 *>(v_new), static_cast<uint4 *>(kv->k),
+      static_cast<uint4 *>(kv->v), n, kv->h_kv, vec, kv->capacity, kv->len);
+  LAUNCH_CHECK("kv_append_kernel");
+  kv->len += n;
+  return MEDHA_OK;
+}
+
+size_t medha_decode_workspace_size(int32_t batch, int32_t h_q, int32_t h_kv, int32_t d) {
+  if (batch <= 0 || h_q <= 0 || h_kv <= 0 || d <= 0) return 256;
+  return decode_ws_layout(batch, h_q, h_kv, d, nullptr, nullptr);
+}
+
+medha_status medha_attn_decode_partial(const medha_kv_shard *kvs_host, int32_t batch, const void *q, int32_t h_q,
+                                       const int64_t *q_pos_host, float scale, float *o, float *lse, void *ws,
+                                       size_t ws_bytes, void *stream) {
+  return decode_partial_impl(kvs_host, batch, q, h_q, q_pos_host, scale, o, lse, ws, ws_bytes,
+                             static_cast<cudaStream_t>(stream));
+}
+
+size_t medha_prefill_workspace_size(int64_t c, int32_t h_q, int32_t h_kv, int32_t d) {
+  (void)h_kv;
+  if (c <= 0 || h_q <= 0 || d <= 0) return 256;
+  return prefill_ws_bound(c, h_q, d);
+}
+
+medha_status medha_attn_prefill_chunk(const medha_kv_shard *kv, const void *q, int64_t c, int32_t h_q, int64_t q_pos0,
+                                      float scale, float *o, float *lse, void *ws, size_t ws_bytes, void *stream) {
+  return prefill_impl(kv, q, c, h_q, q_pos0, scale, o, lse, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+medha_status medha_merge_partials(const float *parts, int32_t P, int64_t rows, int32_t d, float *o_out, float *lse_out,
+                                  void *o_out_bf16, void *stream) {
+  if (!parts || !o_out) return fail(MEDHA_EINVAL, "null argument");
+  if (P < 1 || P > 64) return fail(MEDHA_EINVAL, "P = %d not in [1, 64]", P);
+  if (rows < 0) return fail(MEDHA_EINVAL, "negative rows");
+  if (!supported_d(d)) return fail(MEDHA_ENOTSUP, "head dim %d", d);
+  return merge_impl(parts, P, rows, rows * (d + 1), d, o_out, lse_out, o_out_bf16, static_cast<cudaStream_t>(stream));
+}
+
+// ---- KVP -------------------------------------------------------------------------------------
+medha_status medha_kvp_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return fail(MEDHA_EINVAL, "null id");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(MEDHA_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(id_out, &id, 128);
+  return MEDHA_OK;
+}
+
+medha_status medha_kvp_comm_create(const uint8_t id[128], int32_t rank, int32_t world, medha_kvp_comm **out) {
+  if (!id || !out) return fail(MEDHA_EINVAL, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(MEDHA_EINVAL, "rank %d / world %d", rank, world);
+  ncclUniqueId uid;
+  memcpy(&uid, id, 128);
+  medha_kvp_comm *c = new medha_kvp_comm();
+  c->rank = rank;
+  c->world = world;
+  ncclResult_t r = ncclCommInitRank(&c->nccl, world, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(MEDHA_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return MEDHA_OK;
+}
+
+medha_status medha_kvp_comm_destroy(medha_kvp_comm *comm) {
+  if (!comm) return MEDHA_OK;
+  ncclResult_t r = ncclCommDestroy(comm->nccl);
+  delete comm;
+  if (r != ncclSuccess) return fail(MEDHA_ENCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+  return MEDHA_OK;
+}
+
+medha_status medha_kvp_comm_info(const medha_kvp_comm *comm, int32_t *rank, int32_t *world) {
+  if (!comm) return fail(MEDHA_EINVAL, "null comm");
+  if (rank) *rank = comm->rank;
+  if (world) *world = comm->world;
+  return MEDHA_OK;
+}
+
+static medha_status kvp_exchange_merge(medha_kvp_comm *comm, float *send, float *recv, int64_t rows, int32_t d,
+                                       float *o_out, float *lse_out, void *o_bf16, cudaStream_t st) {
+  const size_t count = (size_t)rows * (d + 1);
+  ncclResult_t r = ncclAllGather(send, recv, count, ncclFloat, comm->nccl, st);
+  if (r != ncclSuccess) return fail(MEDHA_ENCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+  ncclResult_t async_err = ncclSuccess;
+  if (ncclCommGetAsyncError(comm->nccl, &async_err) == ncclSuccess && async_err != ncclSuccess &&
+      async_err != ncclInProgress)
+    return fail(MEDHA_ENCCL, "NCCL async error: %s", ncclGetErrorString(async_err));
+  return merge_impl(recv, comm->world, rows, (int64_t)count, d, o_out, lse_out, o_bf16, st);
+}
+
+static size_t kvp_buf_bytes(int32_t world, int64_t rows, int32_t d) {
+  const size_t count = (size_t)rows * (d + 1);
+  return round_up(count * 4, 256) + round_up(count * 4 * (size_t)world, 256);
+}
+
+size_t medha_kvp_workspace_size(int32_t world, int32_t batch, int32_t h_q, int32_t h_kv, int32_t d) {
+  if (world < 1 || batch <= 0 || h_q <= 0 || d <= 0) return 256;
+  return kvp_buf_bytes(world, (int64_t)batch * h_q, d) + medha_decode_workspace_size(batch, h_q, h_kv, d);
+}
+
+medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_host, int32_t batch, const void *q,
+                              int32_t h_q, const int64_t *q_pos_host, float scale, float *o_out, float *lse_out,
+                              void *o_out_bf16, void *ws, size_t ws_bytes, void *stream) {
+  if (!comm) return fail(MEDHA_EINVAL, "null comm");
+  if (batch <= 0 || !kvs_host) return fail(MEDHA_EINVAL, "empty batch");
+  if (!o_out) return fail(MEDHA_EINVAL, "null o_out");
+  const int32_t d = kvs_host[0].d, h_kv = kvs_host[0].h_kv;
+  if (!supported_d(d)) return fail(MEDHA_ENOTSUP, "head dim %d", d);
+  const int64_t rows = (int64_t)batch * h_q;
+  const size_t need = medha_kvp_workspace_size(comm->world, batch, h_q, h_kv, d);
+  if (!ws || ws_bytes < need) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char *base = static_cast<char *>(ws);
+  const size_t count = (size_t)rows * (d + 1);
+  float *send = reinterpret_cast<float *>(base);
+  float *recv = reinterpret_cast<float *>(base + round_up(count * 4, 256));
+  char *dws = base + kvp_buf_bytes(comm->world, rows, d);
+  medha_status s = decode_partial_impl(kvs_host, batch, q, h_q, q_pos_host, scale, send, send + rows * d, dws,
+                                       ws_bytes - (size_t)(dws - base), st);
+  if (s) return s;
+  return kvp_exchange_merge(comm, send, recv, rows, d, o_out, lse_out, o_out_bf16, st);
+}
+
+size_t medha_kvp_prefill_workspace_size(int32_t world, int64_t c, int32_t h_q, int32_t h_kv, int32_t d) {
+  if (world < 1 || c <= 0 || h_q <= 0 || d <= 0) return 256;
+  return kvp_buf_bytes(world, c * h_q, d) + medha_prefill_workspace_size(c, h_q, h_kv, d);
+}
+
+medha_status medha_kvp_prefill_chunk(medha_kvp_comm *comm, const medha_kv_shard *kv, const void *q, int64_t c,
+                                     int32_t h_q, int64_t q_pos0, float scale, float *o_out, float *lse_out,
+                                     void *o_out_bf16, void *ws, size_t ws_bytes, void *stream) {
+  if (!comm) return fail(MEDHA_EINVAL, "null comm");
+  if (!kv) return fail(MEDHA_EINVAL, "null shard");
+  if (c <= 0) return fail(MEDHA_EINVAL, "empty chunk");
+  if (!o_out) return fail(MEDHA_EINVAL, "null o_out");
+  const int32_t d = kv->d;
+  if (!supported_d(d)) return fail(MEDHA_ENOTSUP, "head dim %d", d);
+  const int64_t rows = c * h_q;
+  const size_t need = medha_kvp_prefill_workspace_size(comm->world, c, h_q, kv->h_kv, d);
+  if (!ws || ws_bytes < need) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char *base = static_cast<char *>(ws);
+  const size_t count = (size_t)rows * (d + 1);
+  float *send = reinterpret_cast<float *>(base);
+  float *recv = reinterpret_cast<float *>(base + round_up(count * 4, 256));
+  char *pws = base + kvp_buf_bytes(comm->world, rows, d);
+  medha_status s = prefill_impl(kv, q, c, h_q, q_pos0, scale, send, send + rows * d, pws,
+                                ws_bytes - (size_t)(pws - base), st);
+  if (s) return s;
+  return kvp_exchange_merge(comm, send, recv, rows, d, o_out, lse_out, o_out_bf16, st);
+}
+
+// ---- end-to-end decode step with host buffers -----------------------------------------------
+size_t medha_decode_step_workspace_size(int32_t world, int32_t h_q, int32_t h_kv, int32_t d) {
+  if (h_q <= 0 || h_kv <= 0 || d <= 0) return 256;
+  const size_t stage = round_up((size_t)h_q * d * 2, 256) + 2 * round_up((size_t)h_kv * d * 2, 256) +
+                       round_up((size_t)h_q * d * 4, 256) + round_up((size_t)h_q * 4, 256);
+  const size_t inner = world > 1 ? medha_kvp_workspace_size(world, 1, h_q, h_kv, d)
+                                 : medha_decode_workspace_size(1, h_q, h_kv, d);
+  return stage + inner;
+}
+
+medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, int32_t append, const void *q_host,
+                                    const void *k_new_host, const void *v_new_host, int32_t h_q, int64_t q_pos,
+                                    float scale, float *o_host, float *lse_host, void *ws, size_t ws_bytes,
+                                    void *stream) {
+  medha_status s = check_shard(kv);
+  if (s) return s;
+  if (!q_host || !o_host) return fail(MEDHA_EINVAL, "null host buffer");
+  if (append && (!k_new_host || !v_new_host)) return fail(MEDHA_EINVAL, "null k/v host buffer");
+  const int32_t d = kv->d, h_kv = kv->h_kv;
+  const int32_t world = comm ? comm->world : 1;
+  const size_t need = medha_decode_step_workspace_size(world, h_q, h_kv, d);
+  if (!ws || ws_bytes < need) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char *b = static_cast<char *>(ws);
+  const size_t qb = (size_t)h_q * d * 2, kb = (size_t)h_kv * d * 2;
+  void *q_dev = b;
+  b += round_up(qb, 256);
+  void *k_dev = b;
+  b += round_up(kb, 256);
+  void *v_dev = b;
+  b += round_up(kb, 256);
+  float *o_dev = reinterpret_cast<float *>(b);
+  b += round_up((size_t)h_q * d * 4, 256);
+  float *lse_dev = reinterpret_cast<float *>(b);
+  b += round_up((size_t)h_q * 4, 256);
+  const size_t rest = ws_bytes - (size_t)(b - static_cast<char *>(ws));
+  CUDA_TRY(cudaMemcpyAsync(q_dev, q_host, qb, cudaMemcpyHostToDevice, st));
+  if (append) {
+    CUDA_TRY(cudaMemcpyAsync(k_dev, k_new_host, kb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(v_dev, v_new_host, kb, cudaMemcpyHostToDevice, st));
+    if ((s = medha_kv_append(kv, k_dev, v_dev, 1, stream))) return s;
+  }
+  const int64_t qp = q_pos;
+  if (comm)
+    s = medha_kvp_decode(comm, kv, 1, q_dev, h_q, &qp, scale, o_dev, lse_dev, nullptr, b, rest, stream);
+  else
+    s = decode_partial_impl(kv, 1, q_dev, h_q, &qp, scale, o_dev, lse_dev, b, rest, st);
+  if (s) return s;
+  CUDA_TRY(cudaMemcpyAsync(o_host, o_dev, (size_t)h_q * d * 4, cudaMemcpyDeviceToHost, st));
+  if (lse_host) CUDA_TRY(cudaMemcpyAsync(lse_host, lse_dev, (size_t)h_q * 4, cudaMemcpyDeviceToHost, st));
+  return MEDHA_OK;
+}
+
+medha_status medha_hbm_read_probe(const void *src, size_t bytes, float *sink, void *stream) {
+  if (!src || !sink) return fail(MEDHA_EINVAL, "null argument");
+  if (!aligned16(src) || (bytes & 15)) return fail(MEDHA_EINVAL, "src/bytes not 16-byte aligned");
+  const int64_t n_vec = (int64_t)(bytes / 16);
+  const int blocks = num_sms() * 4;
+  hbm_read_probe_kernel<<<blocks, 512, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint4 *>(src), n_vec,
+                                                                               sink);
+  LAUNCH_CHECK("hbm_read_probe_kernel");
+  return MEDHA_OK;
+}
+
+}  // extern "C"

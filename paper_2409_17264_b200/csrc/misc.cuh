@@ -1,0 +1,83 @@
+// misc.cuh — K1 kv_append, K5 LSE merge, K6 HBM read probe.
+#pragma once
+#include "common.cuh"
+
+namespace medha {
+
+// K1: scatter n new token-major rows [n][h_kv][D] into the
+// head-major shard [h_kv][cap][D] at local token `len`.  One 16-byte vector per thread.
+__global__ void kv_append_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
+                                 uint4 *__restrict__ k, uint4 *__restrict__ v, int64_t n, int32_t h_kv,
+                                 int32_t vec_per_row, int64_t cap, int64_t len) {
+  const int64_t total = n * h_kv * vec_per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / vec_per_row;          // row = t*h_kv + h
+    const int32_t e = (int32_t)(i - row * vec_per_row);
+    const int64_t t = row / h_kv;
+    const int32_t h = (int32_t)(row - t * h_kv);
+    const int64_t dst = ((int64_t)h * cap + len + t) * vec_per_row + e;
+    k[dst] = k_new[i];
+    v[dst] = v_new[i];
+  }
+}
+
+// K5 ("combined using online-softmax"): part r starts at
+// parts + r*part_stride and holds o [rows][D] then lse [rows] (natural log);
+// part_stride = rows*(D+1) for the packed ABI layout (>= that for padded workspaces).  One warp per row; parts are
+// combined in order r = 0..P-1, so the result does not depend on which rank runs it.
+template <int D>
+__global__ void lse_merge_kernel(const float *__restrict__ parts, int32_t P, int64_t rows, int64_t part_stride,
+                                 float *__restrict__ o_out, float *__restrict__ lse_out,
+                                 __nv_bfloat16 *__restrict__ o_bf16) {
+  constexpr int PER = D / 32;  // floats per lane: d = lane + 32 i (coalesced; parts are packed, no alignment beyond 4 B)
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float *lse_base = parts + rows * D + row;
+  float M = -INFINITY;
+  for (int r = 0; r < P; ++r) M = fmaxf(M, lse_base[(int64_t)r * part_stride]);
+  float acc[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+  float lse = -INFINITY;
+  if (M != -INFINITY) {
+    float s = 0.f;
+    for (int r = 0; r < P; ++r) s += __expf(lse_base[(int64_t)r * part_stride] - M);
+    lse = M + __logf(s);
+    for (int r = 0; r < P; ++r) {
+      const float w = __expf(lse_base[(int64_t)r * part_stride] - lse);
+      const float *orow = parts + (int64_t)r * part_stride + row * D;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) acc[i] += w * orow[lane + 32 * i];
+    }
+  }
+  float *od = o_out + row * D;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) od[lane + 32 * i] = acc[i];
+  if (o_bf16) {
+    __nv_bfloat16 *ob = o_bf16 + row * D;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) ob[lane + 32 * i] = __float2bfloat16_rn(acc[i]);
+  }
+  if (lse_out && lane == 0) lse_out[row] = lse;
+}
+
+// K6: read-only HBM probe (measurement aid).  Grid-stride 16-byte streaming loads.
+__global__ void hbm_read_probe_kernel(const uint4 *__restrict__ src, int64_t n_vec, float *__restrict__ sink) {
+  uint32_t x = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n_vec; i += 4 * stride) {
+    const uint4 a = ldg_stream(src + i), b = ldg_stream(src + i + stride);
+    const uint4 c = ldg_stream(src + i + 2 * stride), d = ldg_stream(src + i + 3 * stride);
+    x ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w ^ d.x ^ d.y ^ d.z ^ d.w;
+  }
+  for (; i < n_vec; i += stride) {
+    const uint4 a = ldg_stream(src + i);
+    x ^= a.x ^ a.y ^ a.z ^ a.w;
+  }
+  x = __reduce_xor_sync(0xffffffffu, x);
+  if ((threadIdx.x & 31) == 0 && x == 0x9E3779B9u) sink[blockIdx.x & 4095] = 1.f;  // practically never taken
+}
+
+}  // namespace medha

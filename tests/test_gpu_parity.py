@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerances are the north_star ones (max-abs 2e-2, mean-abs 2e-3; KVP vs single
+GPU 1e-3 on fp32 outputs).  Query amplitudes are raised (amp 4-8) so softmax is
+peaked and |O| ~ O(1), which is what makes the tolerances bite.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from helpers import (KVP_ABS, compare, default_scale, make_global_kv, oracle_attention, to_shard)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def M():
+    import paper_2409_17264_b200 as M
+    return M
+
+
+# ------------------------------------------------------------------------------------ K1
+def test_kv_append_bit_exact(M):
+    h_kv, d, cap = 3, 128, 50
+    sh = M.KVShard.empty(h_kv, cap, d)
+    sh.k.zero_(); sh.v.zero_()
+    k1 = synth.kv_block(1, 4, 0, 7, h_kv, d).cuda()
+    v1 = synth.kv_block(1, 5, 0, 7, h_kv, d).cuda()
+    M.kv_append(sh, k1, v1)
+    k2 = synth.kv_block(2, 4, 0, 1, h_kv, d).cuda()
+    v2 = synth.kv_block(2, 5, 0, 1, h_kv, d).cuda()
+    M.kv_append(sh, k2, v2)
+    torch.cuda.synchronize()
+    assert sh.len == 8
+    assert torch.equal(sh.k[:, :7], k1.permute(1, 0, 2))
+    assert torch.equal(sh.v[:, 7:8], v2.permute(1, 0, 2))
+    assert torch.count_nonzero(sh.k[:, 8:]) == 0
+    with pytest.raises(M.MedhaError, match="ERANGE"):
+        M.kv_append(sh, torch.zeros((43, h_kv, d), dtype=torch.bfloat16, device="cuda"),
+                    torch.zeros((43, h_kv, d), dtype=torch.bfloat16, device="cuda"))
+
+
+# ------------------------------------------------------------------------------------ K5
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_merge_partials_vs_oracle(M, P):
+    import oracle
+    N, h_kv, G, d = 700, 2, 4, 128
+    k, v = make_global_kv(3, N, h_kv, d)
+    q = synth.queries(3, 5, h_kv * G, d, amp=4.0)
+    qp = [100, 350, 699, 699, 20]
+    cuts = np.linspace(0, N, P + 1).astype(int)
+    parts = [oracle_attention(q, k, v, qp, (int(cuts[r]), int(cuts[r + 1]))) for r in range(P)]
+    rows = 5 * h_kv * G
+    packed = np.concatenate([np.concatenate([o.reshape(-1), l.reshape(-1)]) for o, l in parts]).reshape(P, -1)
+    packed = np.where(np.isneginf(packed), -np.inf, packed)
+    t = torch.from_numpy(packed.astype(np.float32)).cuda()
+    o, lse, ob = M.merge_partials(t, rows, d, want_bf16=True)
+    om, lm = oracle.merge(parts)
+    compare(o.view(5, h_kv * G, d), lse.view(5, h_kv * G), om, lm, max_abs=1e-5, mean_abs=1e-6, lse_abs=1e-5,
+            what="merge")
+    assert torch.equal(ob, o.to(torch.bfloat16))
+
+
+def test_merge_all_empty_rows(M):
+    d, rows = 64, 3
+    parts = torch.zeros((2, rows * (d + 1)), dtype=torch.float32, device="cuda")
+    parts[:, rows * d:] = -float("inf")
+    o, lse, _ = M.merge_partials(parts, rows, d)
+    assert torch.all(o == 0) and torch.all(torch.isneginf(lse))
+
+
+# ------------------------------------------------------------------------------------ K3
+DECODE_CASES = [
+    # (N, h_kv, G, d, amp)
+    (4161, 1, 4, 64, 4.0),     # tiny config decode (configs[0]): KV 4161 incl. own token
+    (1, 2, 4, 128, 4.0),
+    (15, 1, 8, 128, 8.0),
+    (16, 1, 8, 128, 8.0),
+    (17, 2, 2, 64, 8.0),
+    (63, 1, 1, 128, 8.0),
+    (65, 1, 16, 128, 8.0),
+    (1000, 8, 4, 128, 8.0),
+    (3001, 8, 8, 128, 8.0),
+    (5000, 2, 16, 64, 4.0),
+    (40000, 8, 4, 128, 8.0),
+]
+
+
+@pytest.mark.parametrize("N,h_kv,G,d,amp", DECODE_CASES)
+def test_decode_vs_oracle(M, N, h_kv, G, d, amp):
+    k, v = make_global_kv(10 + N, N, h_kv, d)
+    q = synth.queries(10 + N, 1, h_kv * G, d, amp=amp)
+    sh = to_shard(k, v, 0, N)
+    o, lse = M.attn_decode_partial([sh], q.cuda(), [N - 1])
+    om, lm = oracle_attention(q, k, v, [N - 1])
+    compare(o, lse, om, lm, what=f"decode N={N} G={G} d={d}")
+
+
+def test_decode_batch_mixed_lengths_positions(M):
+    """batch > 1 with distinct lengths, shard offsets (pos0), causal cut inside the
+    shard, and a query before the shard (empty -> 0, -inf)."""
+    h_kv, G, d = 2, 4, 128
+    specs = [(0, 300, 299), (1000, 1700, 1699), (50, 2100, 900), (4000, 4100, 3999), (10, 10 + 5000, 10 + 4999)]
+    shards, qs, qps, refs = [], [], [], []
+    for i, (a, b, qpos) in enumerate(specs):
+        k, v = make_global_kv(50 + i, b, h_kv, d)
+        q = synth.queries(50 + i, 1, h_kv * G, d, amp=6.0)
+        shards.append(to_shard(k, v, a, b))
+        qs.append(q)
+        qps.append(qpos)
+        refs.append(oracle_attention(q, k, v, [qpos], (a, b)))
+    o, lse = M.attn_decode_partial(shards, torch.cat(qs).cuda(), qps)
+    for i in range(len(specs)):
+        compare(o[i:i + 1], lse[i:i + 1], refs[i][0], refs[i][1], what=f"batch item {i}")
+    assert torch.all(o[3] == 0) and torch.all(torch.isneginf(lse[3]))
+
+
+def test_decode_large_batch_chunks(M):
+    """batch > 64 sequences exercises the per-launch chunking of the host planner."""
+    h_kv, G, d, B = 1, 4, 64, 70
+    k, v = make_global_kv(77, 600, h_kv, d)
+    q = synth.queries(77, B, h_kv * G, d, amp=4.0)
+    lens = [10 + 7 * i for i in range(B)]
+    shards = [to_shard(k, v, 0, n) for n in lens]
+    o, lse = M.attn_decode_partial(shards, q.cuda(), [n - 1 for n in lens])
+    for i in (0, 33, 63, 64, 69):
+        om, lm = oracle_attention(q[i:i + 1], k[:lens[i]], v[:lens[i]], [lens[i] - 1])
+        compare(o[i:i + 1], lse[i:i + 1], om, lm, what=f"seq {i}")
+
+
+def test_decode_deterministic_and_mask_leak(M):
+    """R13 run-to-run determinism; I10 tokens past len (NaN poison) never leak."""
+    N, h_kv, G, d = 20000, 8, 4, 128
+    k, v = make_global_kv(5, N, h_kv, d)
+    q = synth.queries(5, 1, h_kv * G, d, amp=8.0).cuda()
+    sh = to_shard(k, v, 0, N, extra_cap=300, poison=True)
+    o1, l1 = M.attn_decode_partial([sh], q, [N - 1])
+    o1, l1 = o1.clone(), l1.clone()
+    o2, l2 = M.attn_decode_partial([sh], q, [N - 1])
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    sh.k[:, N:] = 1e4
+    o3, l3 = M.attn_decode_partial([sh], q, [N - 1])
+    assert torch.equal(o1, o3) and torch.equal(l1, l3)
+    # causal cut inside the shard: keys > q_pos never matter (I10)
+    o4, l4 = M.attn_decode_partial([sh], q, [N // 2])
+    sh.v[:, N // 2 + 1:N] = float("nan")
+    o5, l5 = M.attn_decode_partial([sh], q, [N // 2])
+    assert torch.equal(o4, o5) and torch.equal(l4, l5)
+
+
+def test_decode_closed_form_k_zero_large(M):
+    """I12 at 2^20 keys: K = 0 => O = mean(V[0..q_pos]), LSE = ln(q_pos+1)."""
+    N, h_kv, G, d = 1 << 20, 2, 4, 128
+    v = synth.kv_block(9, synth.STREAM_V, 0, N, h_kv, d, device="cuda")
+    K = torch.zeros((h_kv, N, d), dtype=torch.bfloat16, device="cuda")
+    V = v.permute(1, 0, 2).contiguous()
+    from paper_2409_17264_b200 import KVShard
+    sh = KVShard(K, V, N, 0)
+    q = synth.queries(9, 1, h_kv * G, d, amp=8.0).cuda()
+    for qpos in (N - 1, 777_777):
+        o, lse = M.attn_decode_partial([sh], q, [qpos])
+        ref = V[:, :qpos + 1].double().mean(dim=1)                 # [h_kv][d]
+        ref = ref.repeat_interleave(G, dim=0)[None]
+        err = (o.double() - ref).abs()
+        assert err.max().item() < 2e-3, err.max().item()
+        assert torch.allclose(lse.double(), torch.full_like(lse.double(), math.log(qpos + 1)), atol=2e-4)
+
+
+# ------------------------------------------------------------------------------------ K2
+PREFILL_CASES = [
+    # (prefix, c, h_kv, G, d, amp)
+    (4096, 64, 1, 4, 64, 4.0),      # tiny config prefill chunk (configs[0])
+    (0, 1, 1, 4, 128, 4.0),
+    (0, 63, 2, 4, 128, 8.0),
+    (100, 65, 1, 8, 128, 8.0),
+    (257, 200, 2, 1, 128, 6.0),
+    (1000, 129, 1, 2, 64, 6.0),
+    (3000, 40, 2, 16, 128, 8.0),
+    (0, 300, 1, 4, 128, 8.0),
+    (5000, 1024, 2, 4, 128, 8.0),
+    (20000, 96, 8, 4, 128, 8.0),    # small chunk, long prefix -> split-KV path
+]
+
+
+@pytest.mark.parametrize("prefix,c,h_kv,G,d,amp", PREFILL_CASES)
+def test_prefill_vs_oracle(M, prefix, c, h_kv, G, d, amp):
+    N = prefix + c
+    k, v = make_global_kv(200 + c, N, h_kv, d)
+    q = synth.queries(200 + c, c, h_kv * G, d, amp=amp)
+    sh = to_shard(k, v, 0, N)
+    o, lse = M.attn_prefill_chunk(sh, q.cuda(), prefix)
+    qp = list(range(prefix, prefix + c))
+    if c * N > 4_000_000:  # sample rows for the oracle
+        rows = sorted(set([0, 1, c // 3, c // 2, c - 2, c - 1]))
+        om, lm = oracle_attention(q[rows], k, v, [qp[r] for r in rows])
+        compare(o[rows], lse[rows], om, lm, what=f"prefill P0={prefix} c={c}")
+    else:
+        om, lm = oracle_attention(q, k, v, qp)
+        compare(o, lse, om, lm, what=f"prefill P0={prefix} c={c} G={G} d={d}")
+
+
+def test_prefill_chunked_equals_one_shot(M):
+    """I2 on the GPU: chunks of any size over the growing KV equal one-shot causal prefill."""
+    n, h_kv, G, d = 700, 2, 4, 128
+    k, v = make_global_kv(31, n, h_kv, d)
+    q = synth.queries(31, n, h_kv * G, d, amp=6.0).cuda()
+    from paper_2409_17264_b200 import KVShard
+    full = to_shard(k, v, 0, n)
+    o_full, l_full = M.attn_prefill_chunk(full, q, 0)
+    for c in (64, 256):
+        sh = KVShard.empty(h_kv, n + 5, d)
+        outs, lses = [], []
+        for a in range(0, n, c):
+            b = min(n, a + c)
+            M.kv_append(sh, k[a:b].cuda(), v[a:b].cuda())
+            o, l = M.attn_prefill_chunk(sh, q[a:b], a)
+            outs.append(o.clone()); lses.append(l.clone())
+        oc, lc = torch.cat(outs), torch.cat(lses)
+        assert (oc - o_full).abs().max().item() < 1e-3
+        assert (lc - l_full).abs().max().item() < 1e-3
+
+
+def test_decode_equals_last_prefill_row(M):
+    """I9: decode of token n-1 equals the last row of the prefill over n tokens."""
+    n, h_kv, G, d = 900, 2, 8, 128
+    k, v = make_global_kv(41, n, h_kv, d)
+    q = synth.queries(41, 3, h_kv * G, d, amp=6.0).cuda()
+    sh = to_shard(k, v, 0, n)
+    o_p, l_p = M.attn_prefill_chunk(sh, q, n - 3)
+    o_d, l_d = M.attn_decode_partial([sh], q[2:3], [n - 1])
+    assert (o_p[2] - o_d[0]).abs().max().item() < 2e-3
+    assert (l_p[2] - l_d[0]).abs().max().item() < 1e-4
+
+
+# --------------------------------------------------------------------------- KVP on one GPU
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_kvp_emulated_on_one_gpu(M, P):
+    """Single-process KVP: shard one global KV into P contiguous slices, run the
+    partial on each, gather by copy, merge (K5) -> equals single-GPU and oracle."""
+    N, h_kv, G, d = 50000, 8, 4, 128
+    k, v = make_global_kv(60, N, h_kv, d)
+    q = synth.queries(60, 1, h_kv * G, d, amp=8.0)
+    qc = q.cuda()
+    whole = to_shard(k, v, 0, N)
+    o1, l1 = M.attn_decode_partial([whole], qc, [N - 1])
+    o1, l1 = o1.clone(), l1.clone()
+    cuts = [N * r // P for r in range(P + 1)]
+    rows = h_kv * G
+    parts = torch.empty((P, rows * (d + 1)), dtype=torch.float32, device="cuda")
+    for r in range(P):
+        sh = to_shard(k, v, cuts[r], cuts[r + 1])
+        o, l = M.attn_decode_partial([sh], qc, [N - 1])
+        parts[r, :rows * d] = o.reshape(-1)
+        parts[r, rows * d:] = l.reshape(-1)
+    om, lm, _ = M.merge_partials(parts, rows, d)
+    assert (om.view_as(o1) - o1).abs().max().item() <= KVP_ABS
+    assert (lm.view_as(l1) - l1).abs().max().item() <= KVP_ABS
+    ro, rl = oracle_attention(q, k, v, [N - 1])
+    compare(om.view(1, rows, d), lm.view(1, rows), ro, rl, what=f"kvp-emulated P={P}")
+
+
+def test_needle_in_non_tail_shard(M):
+    """I13: a needle key in shard 0 of 4 must dominate after the merge."""
+    N, h_kv, G, d = 8000, 1, 4, 128
+    k = torch.zeros((N, h_kv, d), dtype=torch.bfloat16)
+    v = synth.kv_block(70, synth.STREAM_V, 0, N, h_kv, d)
+    q = synth.queries(70, 1, G, d, amp=2.0)
+    js = 123
+    k[js, 0] = q[0, 0]  # z* = s |q0|^2 for head 0
+    cuts = [0, 2000, 4000, 6000, 8000]
+    rows = G
+    parts = torch.empty((4, rows * (d + 1)), dtype=torch.float32, device="cuda")
+    for r in range(4):
+        sh = to_shard(k, v, cuts[r], cuts[r + 1])
+        o, l = M.attn_decode_partial([sh], q.cuda(), [N - 1])
+        parts[r, :rows * d] = o.reshape(-1)
+        parts[r, rows * d:] = l.reshape(-1)
+    om, lm, _ = M.merge_partials(parts, rows, d)
+    ro, rl = oracle_attention(q, k, v, [N - 1])
+    compare(om.view(1, rows, d), lm.view(1, rows), ro, rl, what="needle")
+    s = 1 / math.sqrt(d)
+    zs = s * float((q[0, 0].double() ** 2).sum())
+    want = (math.exp(zs) * v[js, 0].double() + (v[:, 0].double().sum(0) - v[js, 0].double())) / (math.exp(zs) + N - 1)
+    assert (om.view(rows, d)[0].double().cpu() - want).abs().max().item() < 2e-3
+
+
+# --------------------------------------------------------------------------- errors / ABI
+def test_error_codes(M):
+    sh = M.KVShard.empty(2, 10, 96)  # d = 96 unsupported
+    q = torch.zeros((1, 8, 96), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(M.MedhaError, match="ENOTSUP"):
+        M.attn_decode_partial([sh], q, [0])
+    sh = M.KVShard.empty(3, 10, 128)
+    q = torch.zeros((1, 8, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(M.MedhaError, match="EINVAL"):
+        M.attn_decode_partial([sh], q, [0])   # 8 % 3 != 0
+    sh = M.KVShard.empty(1, 10, 128)
+    q = torch.zeros((1, 32, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(M.MedhaError, match="ENOTSUP"):
+        M.attn_decode_partial([sh], q, [0])   # G = 32
