@@ -169,6 +169,19 @@ medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_ho
                               void *ws, size_t ws_bytes, void *stream);
 
 /*
+ * kvp_exchange_merge (SURVEY a6 + a7 on their own): all-gathers this rank's packed
+ * partial `send` (fp32 [rows*(d+1)]: o [rows][d] then lse [rows], e.g. written by
+ * medha_attn_decode_partial with o = send, lse = send + rows*d) and merges the
+ * world's partials in rank order into o_out / lse_out / o_out_bf16.  ws holds the
+ * receive buffer (medha_kvp_exchange_workspace_size bytes).  medha_kvp_decode is
+ * exactly medha_attn_decode_partial followed by this call.
+ */
+size_t medha_kvp_exchange_workspace_size(int32_t world, int64_t rows, int32_t d);
+medha_status medha_kvp_exchange_merge(medha_kvp_comm *comm, const float *send, int64_t rows, int32_t d,
+                                      float *o_out, float *lse_out, void *o_out_bf16,
+                                      void *ws, size_t ws_bytes, void *stream);
+
+/*
  * kvp_prefill_chunk (Eq. 6): a prefill chunk under KVP — every rank
  * attends the replicated chunk queries over its own shard (ranks whose shard holds
  * no visible key contribute (0, -inf)), then the partials are all-gathered and

@@ -20,7 +20,7 @@ from typing import List, Optional, Sequence
 import torch
 
 __all__ = ["lib", "MedhaError", "KVShard", "kv_append", "attn_decode_partial", "attn_prefill_chunk",
-           "merge_partials", "KVPComm", "kvp_decode", "kvp_prefill_chunk", "decode_step_host",
+           "merge_partials", "KVPComm", "kvp_decode", "kvp_exchange_merge", "exchange_workspace", "kvp_prefill_chunk", "decode_step_host",
            "hbm_read_probe", "decode_workspace", "prefill_workspace", "kvp_workspace", "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmedha_attn.so")
@@ -62,6 +62,8 @@ _sig("medha_kvp_comm_destroy", _i32, _vp)
 _sig("medha_kvp_comm_info", _i32, _vp, _P(_i32), _P(_i32))
 _sig("medha_kvp_workspace_size", _sz, _i32, _i32, _i32, _i32, _i32)
 _sig("medha_kvp_decode", _i32, _vp, _P(_Shard), _i32, _vp, _i32, _P(_i64), _f32, _vp, _vp, _vp, _vp, _sz, _vp)
+_sig("medha_kvp_exchange_workspace_size", _sz, _i32, _i64, _i32)
+_sig("medha_kvp_exchange_merge", _i32, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("medha_kvp_prefill_workspace_size", _sz, _i32, _i64, _i32, _i32, _i32)
 _sig("medha_kvp_prefill_chunk", _i32, _vp, _P(_Shard), _vp, _i64, _i32, _i64, _f32, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("medha_decode_step_workspace_size", _sz, _i32, _i32, _i32, _i32)
@@ -271,6 +273,21 @@ def kvp_decode(comm: KVPComm, shards: Sequence[KVShard], q: torch.Tensor, q_pos:
     _check(lib.medha_kvp_decode(comm.handle, _shards_c(shards), B, _ptr(q), h_q, qp, _scale(scale, d), _ptr(o),
                                 _ptr(lse), _ptr(ob), _ptr(ws), ws.numel(), _stream(stream)), "kvp_decode")
     return o, lse, ob
+
+
+def exchange_workspace(world, rows, d, device=None):
+    return _workspace(f"xchg{world}", lib.medha_kvp_exchange_workspace_size(world, rows, d), device or "cuda")
+
+
+def kvp_exchange_merge(comm: KVPComm, send: torch.Tensor, rows: int, d: int, o_out: torch.Tensor,
+                       lse_out: Optional[torch.Tensor] = None, o_bf16: Optional[torch.Tensor] = None, ws=None,
+                       stream=None) -> None:
+    """a6 + a7: all-gather this rank's packed (o, lse) partial and merge in rank order."""
+    _need_cuda(send, "send", torch.float32)
+    if ws is None:
+        ws = exchange_workspace(comm.world, rows, d, send.device)
+    _check(lib.medha_kvp_exchange_merge(comm.handle, _ptr(send), rows, d, _ptr(o_out), _ptr(lse_out), _ptr(o_bf16),
+                                        _ptr(ws), ws.numel(), _stream(stream)), "kvp_exchange_merge")
 
 
 def kvp_prefill_chunk(comm: KVPComm, shard: KVShard, q: torch.Tensor, q_pos0: int, scale=None, want_bf16=False,

@@ -488,7 +488,7 @@ medha_status medha_kvp_comm_info(const medha_kvp_comm *comm, int32_t *rank, int3
   return MEDHA_OK;
 }
 
-static medha_status kvp_exchange_merge(medha_kvp_comm *comm, float *send, float *recv, int64_t rows, int32_t d,
+static medha_status kvp_exchange_merge(medha_kvp_comm *comm, const float *send, float *recv, int64_t rows, int32_t d,
                                        float *o_out, float *lse_out, void *o_bf16, cudaStream_t st) {
   const size_t count = (size_t)rows * (d + 1);
   ncclResult_t r = ncclAllGather(send, recv, count, ncclFloat, comm->nccl, st);
@@ -503,6 +503,22 @@ static medha_status kvp_exchange_merge(medha_kvp_comm *comm, float *send, float 
 static size_t kvp_buf_bytes(int32_t world, int64_t rows, int32_t d) {
   const size_t count = (size_t)rows * (d + 1);
   return round_up(count * 4, 256) + round_up(count * 4 * (size_t)world, 256);
+}
+
+size_t medha_kvp_exchange_workspace_size(int32_t world, int64_t rows, int32_t d) {
+  if (world < 1 || rows <= 0 || d <= 0) return 256;
+  return round_up((size_t)rows * (d + 1) * 4 * (size_t)world, 256);
+}
+
+medha_status medha_kvp_exchange_merge(medha_kvp_comm *comm, const float *send, int64_t rows, int32_t d, float *o_out,
+                                      float *lse_out, void *o_out_bf16, void *ws, size_t ws_bytes, void *stream) {
+  if (!comm || !send || !o_out) return fail(MEDHA_EINVAL, "null argument");
+  if (rows <= 0) return fail(MEDHA_EINVAL, "rows must be > 0");
+  if (!supported_d(d)) return fail(MEDHA_ENOTSUP, "head dim %d", d);
+  const size_t need = medha_kvp_exchange_workspace_size(comm->world, rows, d);
+  if (!ws || ws_bytes < need) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  return kvp_exchange_merge(comm, send, static_cast<float *>(ws), rows, d, o_out, lse_out, o_out_bf16,
+                            static_cast<cudaStream_t>(stream));
 }
 
 size_t medha_kvp_workspace_size(int32_t world, int32_t batch, int32_t h_q, int32_t h_kv, int32_t d) {
@@ -619,8 +635,8 @@ medha_status medha_hbm_read_probe(const void *src, size_t bytes, float *sink, vo
   if (!src || !sink) return fail(MEDHA_EINVAL, "null argument");
   if (!aligned16(src) || (bytes & 15)) return fail(MEDHA_EINVAL, "src/bytes not 16-byte aligned");
   const int64_t n_vec = (int64_t)(bytes / 16);
-  const int blocks = num_sms() * 4;
-  hbm_read_probe_kernel<<<blocks, 512, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint4 *>(src), n_vec,
+  const int blocks = num_sms() * 8;
+  hbm_read_probe_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint4 *>(src), n_vec,
                                                                                sink);
   LAUNCH_CHECK("hbm_read_probe_kernel");
   return MEDHA_OK;

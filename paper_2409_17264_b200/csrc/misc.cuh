@@ -62,22 +62,30 @@ __global__ void lse_merge_kernel(const float *__restrict__ parts, int32_t P, int
   if (lse_out && lane == 0) lse_out[row] = lse;
 }
 
-// K6: read-only HBM probe (measurement aid).  Grid-stride 16-byte streaming loads.
-__global__ void hbm_read_probe_kernel(const uint4 *__restrict__ src, int64_t n_vec, float *__restrict__ sink) {
+// K6: read-only HBM probe (measurement aid).  Each warp streams contiguous 4 KiB
+// chunks with 8 independent 16-byte loads per lane in flight.
+__global__ void __launch_bounds__(256) hbm_read_probe_kernel(const uint4 *__restrict__ src, int64_t n_vec,
+                                                            float *__restrict__ sink) {
+  constexpr int U = 8;
   uint32_t x = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < n_vec; i += 4 * stride) {
-    const uint4 a = ldg_stream(src + i), b = ldg_stream(src + i + stride);
-    const uint4 c = ldg_stream(src + i + 2 * stride), d = ldg_stream(src + i + 3 * stride);
-    x ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w ^ d.x ^ d.y ^ d.z ^ d.w;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_chunks = n_vec / (32 * U);
+  for (int64_t ch = warp; ch < n_chunks; ch += n_warps) {
+    const uint4 *p = src + ch * (32 * U) + lane;
+    uint4 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = ldg_stream(p + 32 * u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) x ^= a[u].x ^ a[u].y ^ a[u].z ^ a[u].w;
   }
-  for (; i < n_vec; i += stride) {
+  for (int64_t i = n_chunks * 32 * U + warp * 32 + lane; i < n_vec; i += n_warps * 32) {
     const uint4 a = ldg_stream(src + i);
     x ^= a.x ^ a.y ^ a.z ^ a.w;
   }
   x = __reduce_xor_sync(0xffffffffu, x);
-  if ((threadIdx.x & 31) == 0 && x == 0x9E3779B9u) sink[blockIdx.x & 4095] = 1.f;  // practically never taken
+  if (lane == 0 && x == 0x9E3779B9u) sink[blockIdx.x & 4095] = 1.f;  // practically never taken
 }
 
 }  // namespace medha

@@ -23,8 +23,7 @@ def test_header_declares_the_north_star_entry_points():
 
 
 def test_library_loads_and_exports_every_declared_symbol():
-    from paper_2409_17264_b200 import build
-    path = build.build()
+    from paper_2409_17264_b200 import LIB_PATH as path
     lib = ctypes.CDLL(path)
     missing = [n for n in declared_functions() if not hasattr(lib, n)]
     assert not missing, f"not exported: {missing}"
@@ -47,8 +46,7 @@ def test_status_strings_without_gpu():
 def test_kernels_are_sm100a_and_use_tcgen05_tma():
     """The fatbin holds sm_100a SASS; the prefill kernel uses UTCHMMA (tcgen05.mma),
     LDTM/STTM (tcgen05.ld/st) and UTMALDG (TMA)."""
-    from paper_2409_17264_b200 import build
-    path = build.build()
+    from paper_2409_17264_b200 import LIB_PATH as path
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", path], capture_output=True, text=True).stdout
     assert "sm_100a" in sass
     assert "UTCHMMA" in sass or "UTCMMA" in sass
