@@ -1,7 +1,7 @@
 // medha_attn.cu — host side of libmedha_attn (C ABI declared in include/medha_attn.h).
 // Validation, work planning (split-KV sizing to the SM count), TMA descriptor
 // encoding, NCCL KVP communicator and the all-gather + merge orchestration.
-// Every compute step runs in the kernels of decode.cuh / prefill_tc.cuh / misc.cuh.
+// Every compute step runs in the kernels of decode.cuh / prefill_ws.cuh / misc.cuh.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -17,7 +17,7 @@
 #include "medha_attn.h"
 #include "decode.cuh"
 #include "misc.cuh"
-#include "prefill_tc.cuh"
+#include "prefill_ws.cuh"
 
 using namespace medha;
 
@@ -235,28 +235,41 @@ medha_status make_map_3d(CUtensorMap *m, const void *base, uint64_t d0, uint64_t
 }
 
 struct PrefillPlan {
-  int m_tiles, n_split, tiles_per_split;
+  int m_pairs, n_split, tiles_per_split;
   int64_t rows, part_stride;
   size_t ws_bytes;
 };
 
+// Grid = (query-tile pairs) x (kv heads) x (KV splits).  The split count is chosen to
+// minimise an estimate of the makespan: waves x KV tiles per CTA (wave quantisation on
+// the SM count) plus the HBM time of writing and merging split partials.
 PrefillPlan plan_prefill(int64_t c, int32_t h_q, int32_t h_kv, int32_t d, int64_t n_kv_max) {
   PrefillPlan pl;
   const int G = h_kv > 0 ? std::max(1, h_q / h_kv) : 1;
-  const int TQ = kTileM / std::max(1, std::min(G, kTileM));
-  pl.m_tiles = (int)cdiv(std::max<int64_t>(c, 1), TQ);
+  const int TQ = kWsTileM / std::max(1, std::min(G, kWsTileM));
+  pl.m_pairs = (int)cdiv(std::max<int64_t>(c, 1), 2 * TQ);
   pl.rows = c * h_q;
   pl.part_stride = (int64_t)round_up((size_t)(pl.rows * (d + 1)), 4);
-  const int64_t kv_tiles = std::max<int64_t>(1, cdiv(n_kv_max, kTileN));
-  const int64_t base_ctas = (int64_t)pl.m_tiles * h_kv;
+  const int64_t kv_tiles = std::max<int64_t>(1, cdiv(n_kv_max, kWsTileN));
+  const int64_t base = (int64_t)pl.m_pairs * h_kv;
   const int sms = num_sms();
-  int ns = 1;
-  if (base_ctas < sms) {
-    // split the KV range until the grid fills the GPU, keeping >= 4 KV tiles per split
-    ns = (int)std::min<int64_t>(cdiv(sms, base_ctas), std::max<int64_t>(1, kv_tiles / 4));
-    ns = std::max(1, std::min(ns, 64));
+  const double t_tile_us = 1.2;                                   // ~2x1024 MMA clk per KV tile and pair
+  const double merge_us_per_split = (double)pl.rows * (d + 1) * 4 * 2 / 6.0e6;  // write + read at ~6 TB/s
+  double best = 1e300;
+  int best_ns = 1;
+  for (int ns = 1; ns <= 64; ++ns) {
+    const int64_t tps = cdiv(kv_tiles, ns);
+    const int64_t ns_eff = cdiv(kv_tiles, tps);
+    if (ns_eff != ns) continue;
+    if (ns > 1 && tps < 4) break;
+    const int64_t waves = cdiv(base * ns, sms);
+    const double est = (double)waves * tps * t_tile_us + (ns > 1 ? merge_us_per_split * ns : 0.0);
+    if (est < best * 0.999) {
+      best = est;
+      best_ns = ns;
+    }
   }
-  pl.tiles_per_split = (int)cdiv(kv_tiles, ns);
+  pl.tiles_per_split = (int)cdiv(kv_tiles, best_ns);
   pl.n_split = (int)cdiv(kv_tiles, pl.tiles_per_split);
   pl.ws_bytes = pl.n_split > 1 ? (size_t)pl.n_split * pl.part_stride * sizeof(float) : 0;
   return pl;
@@ -269,21 +282,21 @@ size_t prefill_ws_bound(int64_t c, int32_t h_q, int32_t d) {
 
 template <int D, int G>
 medha_status launch_prefill(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv,
-                            const PrefillParams &p, dim3 grid, cudaStream_t st) {
-  using L = PrefillLayout<D>;
+                            const PrefillWsParams &p, dim3 grid, cudaStream_t st) {
+  using L = WsLayout<D>;
   static bool attr_done = false;
   if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(prefill_tc_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kAlloc));
+    CUDA_TRY(cudaFuncSetAttribute(prefill_ws_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kAlloc));
     attr_done = true;
   }
-  prefill_tc_kernel<D, G><<<grid, kPrefillThreads, L::kAlloc, st>>>(mq, mk, mv, p);
-  LAUNCH_CHECK("prefill_tc_kernel");
+  prefill_ws_kernel<D, G><<<grid, kWsThreads, L::kAlloc, st>>>(mq, mk, mv, p);
+  LAUNCH_CHECK("prefill_ws_kernel");
   return MEDHA_OK;
 }
 
 template <int D>
 medha_status dispatch_prefill_g(int G, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv,
-                                const PrefillParams &p, dim3 grid, cudaStream_t st) {
+                                const PrefillWsParams &p, dim3 grid, cudaStream_t st) {
   switch (G) {
     case 1: return launch_prefill<D, 1>(mq, mk, mv, p, grid, st);
     case 2: return launch_prefill<D, 2>(mq, mk, mv, p, grid, st);
@@ -332,14 +345,14 @@ medha_status prefill_impl(const medha_kv_shard *kv, const void *q, int64_t c, in
     if (ws_bytes < pl.ws_bytes) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, pl.ws_bytes);
   }
   CUtensorMap mq, mk, mv;
-  const int TQ = kTileM / G;
+  const int TQ = kWsTileM / G;
   if ((s = make_map_3d(&mq, q, d, h_q, c, (uint64_t)d * 2, (uint64_t)h_q * d * 2, 64, G, TQ))) return s;
   const uint64_t len_ext = (uint64_t)std::max<int64_t>(kv->len, 1);
-  if ((s = make_map_3d(&mk, kv->k, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64, kTileN, 1)))
+  if ((s = make_map_3d(&mk, kv->k, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64, kWsTileN, 1)))
     return s;
-  if ((s = make_map_3d(&mv, kv->v, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64, kTileN, 1)))
+  if ((s = make_map_3d(&mv, kv->v, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64, kWsTileN, 1)))
     return s;
-  PrefillParams p;
+  PrefillWsParams p;
   memset(&p, 0, sizeof(p));
   p.o = pl.n_split > 1 ? static_cast<float *>(ws) : o;
   p.lse = lse;
@@ -354,7 +367,7 @@ medha_status prefill_impl(const medha_kv_shard *kv, const void *q, int64_t c, in
   p.n_split = pl.n_split;
   p.tiles_per_split = pl.tiles_per_split;
   p.scale_log2 = scale * kLog2e;
-  dim3 grid(pl.m_tiles, h_kv, pl.n_split);
+  dim3 grid(pl.m_pairs, h_kv, pl.n_split);
   s = (d == 128) ? dispatch_prefill_g<128>(G, mq, mk, mv, p, grid, st) : dispatch_prefill_g<64>(G, mq, mk, mv, p, grid, st);
   if (s) return s;
   if (pl.n_split > 1) return merge_impl(static_cast<float *>(ws), pl.n_split, pl.rows, pl.part_stride, d, o, lse, nullptr, st);

@@ -1,0 +1,341 @@
+// prefill_ws.cuh — K2 chunked-prefill partial attention, warp-specialised tcgen05 pipeline.
+// SURVEY.md §8(a) a4 (+ a5 split-KV merge via K5 when the KV range is split).
+//
+// P:352-366 (Eq. 3): a chunk of c query tokens over its KV prefix has arithmetic
+// intensity c*h_q/h_kv, tensor-core bound on B200 once c*G >= ~255.  P:357-358 GQA:
+// the G query heads of one KV head are packed as MMA rows (row = t_local*G + h), so
+// each K/V tile read from HBM feeds all rows of the CTA.
+//
+// One CTA = two 128-row query tiles (A, B) of one KV head and a contiguous range of
+// 128-token KV tiles.  12 warps:
+//   warp 0      TMA producer (one elected lane): Q_A, Q_B once; K_j, V_j through a
+//               4-slot smem ring (full/empty mbarriers).
+//   warp 1      MMA issuer (one elected lane), in the order
+//                 S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...
+//               S = Q K^T (SS, K-major, SWIZZLE_128B) into TMEM; O += P V with P read
+//               from TMEM (TS form; P aliases the first 64 columns of S) and V as an
+//               MN-major smem operand.  tcgen05.commit -> mbarriers.
+//   warp 2      TMEM allocator (512 columns: S_A | S_B | O_A | O_B).
+//   warps 4-7   softmax of tile A, warps 8-11 softmax of tile B: thread = TMEM lane =
+//               query row.  Two passes over S (row max, then exp2/sum/pack), P as bf16
+//               back into TMEM with tcgen05.st.  The running max is only raised when
+//               it grows by more than 2^8 (exact: numerator and denominator use the
+//               same stale max; p <= 256 stays finite in bf16/fp32), so O is rarely
+//               rescaled; when it is, the softmax warps rescale O_X in TMEM.
+// Ordering argument: the commit that publishes S_X(j+1) also covers PV_X(j) (all prior
+// MMAs of the issuing thread), so once a softmax warp sees S_X(j+1) it may overwrite
+// the P columns and rescale O_X.  Tile A's softmax overlaps tile B's MMAs and v.v.
+#pragma once
+#include <cuda.h>
+#include "common.cuh"
+
+namespace medha {
+
+constexpr int kWsThreads = 384;
+constexpr int kWsTileM = 128;
+constexpr int kWsTileN = 128;
+constexpr int kWsSlots = 4;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct PrefillWsParams {
+  float *o;        // [c][h_q][D] (n_split == 1) or ws parts [n_split][part_stride]
+  float *lse;      // [c][h_q]    (n_split == 1)
+  int64_t c;
+  int64_t len;
+  int64_t pos0;
+  int64_t q_pos0;
+  int64_t rows;         // c * h_q
+  int64_t part_stride;  // floats between split parts (multiple of 4)
+  int32_t h_q;
+  int32_t h_kv;
+  int32_t n_split;
+  int32_t tiles_per_split;
+  float scale_log2;
+};
+
+template <int D>
+struct WsLayout {
+  static constexpr uint32_t kHalf = 128 * 64 * 2;    // [128][64] bf16 SW128 block, 16 KiB
+  static constexpr uint32_t kQBytes = kWsTileM * D * 2;
+  static constexpr uint32_t kSlotBytes = kWsTileN * D * 2;
+  static constexpr uint32_t kQ0 = 0;
+  static constexpr uint32_t kSlot0 = 2 * kQBytes;
+  static constexpr uint32_t kBar = kSlot0 + kWsSlots * kSlotBytes;
+  static constexpr uint32_t kTotal = kBar + 256;
+  static constexpr uint32_t kAlloc = kTotal + 1024;
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    prefill_ws_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ PrefillWsParams p) {
+  static_assert(D == 64 || D == 128, "D");
+  static_assert(kWsTileM % G == 0, "G");
+  using L = WsLayout<D>;
+  constexpr int TQ = kWsTileM / G;
+  constexpr int NH = D / 64;
+  constexpr uint32_t kIdescS = umma_idesc_bf16(kWsTileM, kWsTileN, 0);
+  constexpr uint32_t kIdescO = umma_idesc_bf16(kWsTileM, D, 1);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kBar);
+  uint64_t *bar_q = bars + 0;
+  uint64_t *bar_full = bars + 1;              // [4]
+  uint64_t *bar_empty = bars + 5;             // [4]
+  uint64_t *bar_s = bars + 9;                 // [2]
+  uint64_t *bar_p = bars + 11;                // [2]
+  uint64_t *bar_o = bars + 13;                // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 16);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int pair = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
+  const int64_t t0 = (int64_t)pair * 2 * TQ;                 // first query token of tile A
+  const int64_t t1 = min64(p.c, t0 + 2 * TQ);
+  const int64_t n_kv = max64(0, min64(p.len, p.q_pos0 + t1 - 1 - p.pos0 + 1));
+  const int n_tiles_total = (int)((n_kv + kWsTileN - 1) / kWsTileN);
+  const int jt0 = split * p.tiles_per_split;
+  const int n = max(0, min(p.tiles_per_split, n_tiles_total - jt0));
+
+  if (tid == 0) {
+    mbar_init(bar_q, 1);
+    for (int i = 0; i < kWsSlots; ++i) {
+      mbar_init(bar_full + i, 1);
+      mbar_init(bar_empty + i, 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(bar_s + x, 1);
+      mbar_init(bar_p + x, 128);
+      mbar_init(bar_o + x, 1);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  uint8_t *sQ = smem + L::kQ0;
+  auto slot_ptr = [&](int s) { return smem + L::kSlot0 + s * L::kSlotBytes; };
+
+  if (warp == 0) {
+    // ================================ TMA producer ================================
+    if (lane == 0 && n > 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      mbar_arrive_expect_tx(bar_q, 2 * L::kQBytes);
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh)
+          tma_load_3d(sQ + x * L::kQBytes + hh * L::kHalf, &tm_q, bar_q, 64 * hh, kvh * G, (int32_t)(t0 + x * TQ));
+      for (int it = 0; it < 2 * n; ++it) {
+        const int s = it % kWsSlots;
+        if (it >= kWsSlots) mbar_wait(bar_empty + s, ((it / kWsSlots) - 1) & 1);
+        mbar_arrive_expect_tx(bar_full + s, L::kSlotBytes);
+        const int32_t tok = (jt0 + (it >> 1)) * kWsTileN;
+        const void *map = (it & 1) ? (const void *)&tm_v : (const void *)&tm_k;
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) tma_load_3d(slot_ptr(s) + hh * L::kHalf, map, bar_full + s, 64 * hh, tok, kvh);
+      }
+    }
+  } else if (warp == 1) {
+    // ================================ MMA issuer ==================================
+    if (lane == 0 && n > 0) {
+      auto wait_full = [&](int it) {
+        mbar_wait(bar_full + (it % kWsSlots), (it / kWsSlots) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int x, int it) {
+        const uint32_t kb = smem_u32(slot_ptr(it % kWsSlots));
+        const uint32_t qb = smem_u32(sQ + x * L::kQBytes);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks >> 2) * L::kHalf + (ks & 3) * 32;
+          umma_f16_ss(tmem + x * 128, umma_desc_sw128(qb + off, 16, 1024), umma_desc_sw128(kb + off, 16, 1024),
+                      kIdescS, ks > 0);
+        }
+      };
+      auto issue_pv = [&](int x, int it, bool acc) {
+        const uint32_t vb = smem_u32(slot_ptr(it % kWsSlots));
+#pragma unroll
+        for (int ks = 0; ks < kWsTileN / 16; ++ks)
+          umma_f16_ts(tmem + 256 + x * 128, tmem + x * 128 + ks * 8, umma_desc_sw128(vb + ks * 2048, L::kHalf, 1024),
+                      kIdescO, (acc || ks > 0) ? 1u : 0u);
+      };
+      mbar_wait(bar_q, 0);
+      tc_fence_after();
+      wait_full(0);
+      issue_s(0, 0);
+      umma_commit(bar_s + 0);
+      issue_s(1, 0);
+      umma_commit(bar_s + 1);
+      umma_commit(bar_empty + 0);
+      for (int j = 0; j < n; ++j) {
+        const int iv = 2 * j + 1, ik = 2 * j + 2;
+        wait_full(iv);
+        mbar_wait(bar_p + 0, j & 1);
+        tc_fence_after();
+        issue_pv(0, iv, j > 0);
+        if (j == n - 1) umma_commit(bar_o + 0);
+        if (j + 1 < n) {
+          wait_full(ik);
+          issue_s(0, ik);
+          umma_commit(bar_s + 0);
+        }
+        mbar_wait(bar_p + 1, j & 1);
+        tc_fence_after();
+        issue_pv(1, iv, j > 0);
+        umma_commit(bar_empty + (iv % kWsSlots));
+        if (j == n - 1) umma_commit(bar_o + 1);
+        if (j + 1 < n) {
+          issue_s(1, ik);
+          umma_commit(bar_s + 1);
+          umma_commit(bar_empty + (ik % kWsSlots));
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ================================ softmax + epilogue ==========================
+    const int x = (warp - 4) >> 2;          // 0: tile A, 1: tile B
+    const int r = tid - 128 - x * 128;      // row in tile = TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_base + x * 128;
+    const uint32_t tO = tmem + lane_base + 256 + x * 128;
+    const int64_t tx0 = t0 + x * TQ;        // first token of this tile
+    const int64_t t = tx0 + r / G;
+    const int h = kvh * G + r % G;
+    const bool row_valid = t < p.c;
+    const int64_t lenm1 = p.len - 1;
+    const int64_t j_lim = row_valid ? min64(p.q_pos0 + t - p.pos0, lenm1) : -1;
+    // tiles whose last key is <= the smallest j_lim of this query tile need no mask
+    const int64_t j_lim_tile = min64(p.q_pos0 + tx0 - p.pos0, lenm1);
+    const float sl2 = p.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(bar_s + x, j & 1);
+      __syncwarp();
+      tc_fence_after();
+      const int64_t jb = (int64_t)(jt0 + j) * kWsTileN;
+      const bool full = (jb + kWsTileN - 1) <= j_lim_tile;
+      const int nvalid = full ? kWsTileN : (int)min64(kWsTileN, max64(0, j_lim - jb + 1));
+      // ---- pass 1: row max -------------------------------------------------------
+      float mx = -INFINITY;
+#pragma unroll
+      for (int q2 = 0; q2 < 4; q2 += 2) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(tS + 32 * q2, ra);
+        tmem_ld32(tS + 32 * (q2 + 1), rb);
+        tmem_wait_ld();
+        if (full) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, fmaxf(__uint_as_float(ra[e]), __uint_as_float(rb[e])));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (32 * q2 + e < nvalid) mx = fmaxf(mx, __uint_as_float(ra[e]));
+            if (32 * (q2 + 1) + e < nvalid) mx = fmaxf(mx, __uint_as_float(rb[e]));
+          }
+        }
+      }
+      const float m_tile = mx * sl2;
+      float m_use = m_run, alpha = 1.f;
+      bool rescale = false;
+      if (m_tile > m_run + kRescaleThreshold || (m_run == -INFINITY && m_tile != -INFINITY)) {
+        m_use = m_tile;
+        alpha = fast_exp2(m_run - m_tile);   // 0 when m_run = -inf
+        rescale = (j > 0) && (m_run != -INFINITY);
+      }
+      m_run = m_use;
+      const float mu = (m_use == -INFINITY) ? 0.f : m_use;
+      // ---- O rescale (PV_X(j-1) is complete: covered by the S_X(j) commit) ----------
+      if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int q = 0; q < D / 32; ++q) {
+          uint32_t ro[32];
+          tmem_ld32(tO + 32 * q, ro);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ro[e] = __float_as_uint(__uint_as_float(ro[e]) * alpha);
+          tmem_st32(tO + 32 * q, ro);
+        }
+      }
+      // ---- pass 2: P = exp2(s*scale - m) -> bf16 -> TMEM (aliasing S) ------------
+      float lsum = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t ra[32];
+        tmem_ld32(tS + 32 * q, ra);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float p0 = fast_exp2(fmaf(__uint_as_float(ra[e]), sl2, -mu));
+          float p1 = fast_exp2(fmaf(__uint_as_float(ra[e + 1]), sl2, -mu));
+          if (!full) {
+            p0 = (32 * q + e < nvalid) ? p0 : 0.f;
+            p1 = (32 * q + e + 1 < nvalid) ? p1 : 0.f;
+          }
+          lsum += p0 + p1;
+          pk[e >> 1] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(tS + 16 * q, pk);
+      }
+      l_run = l_run * alpha + lsum;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar_p + x);
+    }
+
+    // ---- epilogue --------------------------------------------------------------------
+    const bool has = (n > 0) && (l_run > 0.f);
+    const float inv_l = has ? 1.f / l_run : 0.f;
+    const float lse_nat = has ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+    if (n > 0) {
+      mbar_wait(bar_o + x, 0);
+      __syncwarp();
+      tc_fence_after();
+    }
+    const int64_t grow = t * p.h_q + h;
+    float *orow, *lrow;
+    if (p.n_split == 1) {
+      orow = p.o + grow * D;
+      lrow = p.lse + grow;
+    } else {
+      float *part = p.o + (int64_t)split * p.part_stride;
+      orow = part + grow * D;
+      lrow = part + p.rows * D + grow;
+    }
+#pragma unroll
+    for (int q = 0; q < D / 32; ++q) {
+      uint32_t ro[32];
+      if (n > 0) {
+        tmem_ld32(tO + 32 * q, ro);
+        tmem_wait_ld();
+      }
+      if (row_valid) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          float4 v4;
+          v4.x = has ? __uint_as_float(ro[e]) * inv_l : 0.f;
+          v4.y = has ? __uint_as_float(ro[e + 1]) * inv_l : 0.f;
+          v4.z = has ? __uint_as_float(ro[e + 2]) * inv_l : 0.f;
+          v4.w = has ? __uint_as_float(ro[e + 3]) * inv_l : 0.f;
+          *reinterpret_cast<float4 *>(orow + 32 * q + e) = v4;
+        }
+      }
+    }
+    if (row_valid) *lrow = lse_nat;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace medha

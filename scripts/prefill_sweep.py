@@ -1,0 +1,11 @@
+"""Prefill-chunk TFLOP/s sweep (configs[2]) using bench.py's measurement code."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import bench
+import paper_2409_17264_b200 as M
+pre = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "131072,1048576").split(",")]
+cs = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "64,256,1024,4096").split(",")]
+sh = bench.build_shard(M, 0, 1, max(pre) + max(cs), bench.H_KV, bench.D)
+for r in bench.bench_prefill(M, sh, pre, cs):
+    print(json.dumps(r), flush=True)

@@ -231,7 +231,12 @@ def test_decode_equals_last_prefill_row(M):
     sh = to_shard(k, v, 0, n)
     o_p, l_p = M.attn_prefill_chunk(sh, q, n - 3)
     o_d, l_d = M.attn_decode_partial([sh], q[2:3], [n - 1])
-    assert (o_p[2] - o_d[0]).abs().max().item() < 2e-3
+    ro, rl = oracle_attention(q[2:3].cpu(), k, v, [n - 1])
+    compare(o_p[2:3], l_p[2:3], ro, rl, what="prefill last row")
+    compare(o_d, l_d, ro, rl, what="decode")
+    # the two GPU paths round P to bf16 independently: each is within the oracle
+    # tolerance, so they agree within twice that
+    assert (o_p[2] - o_d[0]).abs().max().item() < 2 * 2e-2
     assert (l_p[2] - l_d[0]).abs().max().item() < 1e-4
 
 
