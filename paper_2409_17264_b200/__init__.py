@@ -235,14 +235,10 @@ class KVPComm:
 
     def __init__(self, group=None):
         import torch.distributed as dist
+        from .kvp import exchange_unique_id
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        buf = (ctypes.c_uint8 * 128)()
-        if self.rank == 0:
-            _check(lib.medha_kvp_unique_id(buf), "kvp_unique_id")
-        obj = [bytes(buf)]
-        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
-        uid = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(exchange_unique_id(group))
         h = ctypes.c_void_p()
         _check(lib.medha_kvp_comm_create(uid, self.rank, self.world, ctypes.byref(h)), "kvp_comm_create")
         self.handle = h
