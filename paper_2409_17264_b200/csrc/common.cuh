@@ -31,6 +31,11 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
+// sum of the two bf16 halves of a packed pair, in fp32 (the exact values the MMA consumes)
+__device__ __forceinline__ float bf16x2_sum(uint32_t u) {
+  return __uint_as_float(u << 16) + __uint_as_float(u & 0xffff0000u);
+}
+
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
@@ -41,6 +46,13 @@ __device__ __forceinline__ float fast_exp2(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
+}
+
+// 2^k for an integer-valued float k (k = -inf or k < -126 -> 0): an exact power of two.
+// Running maxima are kept integer-valued (log2 units), so every rescale is exact and the
+// bf16 rounding of P = 2^(s - m) does not depend on where the KV range was split.
+__device__ __forceinline__ float exp2_int(float k) {
+  return (k < -126.f) ? 0.f : __int_as_float(((int)k + 127) << 23);
 }
 
 // D(16x8 f32) += A(16x16 bf16, row) * B(16x8 bf16, col)   (legacy warp MMA)

@@ -170,15 +170,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
       mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
       mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
     }
-    const float mn_lo = fmaxf(m_lo, mx_lo);
+    // integer-valued running max (log2 units): rescales are exact powers of two
+    const float mn_lo = fmaxf(m_lo, ceilf(mx_lo));
     const float mu_lo = (mn_lo == -INFINITY) ? 0.f : mn_lo;
-    const float al_lo = fast_exp2(m_lo - mu_lo);  // m_lo = -inf -> 0
+    const float al_lo = exp2_int(m_lo - mu_lo);  // m_lo = -inf -> 0
     m_lo = mn_lo;
     float mu_hi = 0.f, al_hi = 1.f;
     if (kHi) {
-      const float mn_hi = fmaxf(m_hi, mx_hi);
+      const float mn_hi = fmaxf(m_hi, ceilf(mx_hi));
       mu_hi = (mn_hi == -INFINITY) ? 0.f : mn_hi;
-      al_hi = fast_exp2(m_hi - mu_hi);
+      al_hi = exp2_int(m_hi - mu_hi);
       m_hi = mn_hi;
     }
     float pr[2][4];
@@ -189,8 +190,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
       pr[n][2] = kHi ? fast_exp2(s[n][2] - mu_hi) : 0.f;
       pr[n][3] = kHi ? fast_exp2(s[n][3] - mu_hi) : 0.f;
     }
-    l_lo = l_lo * al_lo + (pr[0][0] + pr[0][1] + pr[1][0] + pr[1][1]);
-    if (kHi) l_hi = l_hi * al_hi + (pr[0][2] + pr[0][3] + pr[1][2] + pr[1][3]);
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       oacc[j][0] *= al_lo;
@@ -205,6 +204,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     const uint32_t a1 = kHi ? pack_bf16x2(pr[0][2], pr[0][3]) : 0u;
     const uint32_t a2 = pack_bf16x2(pr[1][0], pr[1][1]);
     const uint32_t a3 = kHi ? pack_bf16x2(pr[1][2], pr[1][3]) : 0u;
+    // the normaliser sums the bf16-rounded P the MMA consumes (consistent weights)
+    l_lo = l_lo * al_lo + (bf16x2_sum(a0) + bf16x2_sum(a2));
+    if (kHi) l_hi = l_hi * al_hi + (bf16x2_sum(a1) + bf16x2_sum(a3));
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const int ch = j >> 3, e = j & 7;
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     if (M != -INFINITY) {
 #pragma unroll
       for (int w = 0; w < kDecodeWarps; ++w) {
-        const float sc = fast_exp2(sm_m[w][row] - M);
+        const float sc = exp2_int(sm_m[w][row] - M);
         L += sm_l[w][row] * sc;
         acc += sm_o[w][row][dd] * sc;
       }

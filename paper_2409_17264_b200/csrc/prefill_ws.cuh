@@ -243,12 +243,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           }
         }
       }
-      const float m_tile = mx * sl2;
+      const float m_tile = ceilf(mx * sl2);   // integer-valued (log2 units): exact rescales
       float m_use = m_run, alpha = 1.f;
       bool rescale = false;
       if (m_tile > m_run + kRescaleThreshold || (m_run == -INFINITY && m_tile != -INFINITY)) {
         m_use = m_tile;
-        alpha = fast_exp2(m_run - m_tile);   // 0 when m_run = -inf
+        alpha = exp2_int(m_run - m_tile);   // 0 when m_run = -inf
         rescale = (j > 0) && (m_run != -INFINITY);
       }
       m_run = m_use;
@@ -281,8 +281,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             p0 = (32 * q + e < nvalid) ? p0 : 0.f;
             p1 = (32 * q + e + 1 < nvalid) ? p1 : 0.f;
           }
-          lsum += p0 + p1;
           pk[e >> 1] = pack_bf16x2(p0, p1);
+          lsum += bf16x2_sum(pk[e >> 1]);   // normaliser of the rounded P (consistent weights)
         }
         tmem_st16(tS + 16 * q, pk);
       }

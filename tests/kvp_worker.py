@@ -56,7 +56,7 @@ def main():
     if dmax > 1e-3 or (lse - l1).abs().max().item() > 1e-3:
         fails.append(f"kvp vs single gpu {dmax}")
     if rank == 0:
-        ro, rl = oracle_attention(q, k[:, :2], v[:, :2], qp)            # kv heads 0,1 (8 q heads)
+        ro, rl = oracle_attention(q[:, :2 * G], k[:, :2], v[:, :2], qp)   # kv heads 0,1 (8 q heads)
         try:
             compare(o[:, :2 * G], lse[:, :2 * G], ro, rl, what=f"kvp_decode P={world}")
         except AssertionError as e:
@@ -72,7 +72,8 @@ def main():
                        k[N - 1].contiguous().pin_memory() if tail else None,
                        v[N - 1].contiguous().pin_memory() if tail else None, N - 1, o_h, l_h, ws)
     torch.cuda.synchronize()
-    if not torch.equal(o_h, o[0].cpu()):
+    # (the batch-2 call above planned its KV splits for two sequences: fp32 summation order differs)
+    if (o_h - o[0].cpu()).abs().max().item() > 1e-4:
         fails.append(f"decode_step_host differs from kvp_decode: {(o_h - o[0].cpu()).abs().max().item()}")
 
     # ---- prefill chunk under KVP: Eq. 6 ------------------------------------------------
@@ -87,7 +88,7 @@ def main():
         fails.append(f"kvp prefill vs single gpu {dmax}")
     if rank == 0:
         rows = [0, 100, 255]
-        ro, rl = oracle_attention(qc[rows], k[:, :1], v[:, :1], [N - c + r for r in rows])
+        ro, rl = oracle_attention(qc[rows][:, :G], k[:, :1], v[:, :1], [N - c + r for r in rows])
         try:
             compare(op[rows][:, :G], lp[rows][:, :G], ro, rl, what=f"kvp_prefill P={world}")
         except AssertionError as e:
