@@ -29,6 +29,7 @@
 namespace medha {
 
 constexpr int kDecodeMaxSeqPerLaunch = 64;
+constexpr int kDecodeMaxSplits = 256;  // per (seq, kv head): the merge weights live in sm_o
 constexpr int kDecodeWarps = 4;
 constexpr int kDecodeThreads = kDecodeWarps * 32;
 
@@ -292,22 +293,46 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
   if (sm_ticket != (unsigned)(S.n_splits - 1)) return;
   __threadfence();
   const int64_t slot0 = (int64_t)S.slot_begin + (int64_t)kvh * S.n_splits;
-  const int ns = S.n_splits;
-  for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
-    const int row = idx / D, dd = idx - row * D;
+  const int ns = S.n_splits;                 // <= kDecodeMaxSplits (host planner)
+  float *smw = &sm_o[0][0][0];               // [ns][G] merge weights; warp partials are dead
+  for (int i = tid; i < ns * G; i += kDecodeThreads) smw[i] = __ldcg(p.ws_lse + slot0 * G + i);
+  __syncthreads();
+  // per row: M = max_s lse_s, w_s = 2^(lse_s - M) / sum_s 2^(lse_s - M)   (one warp per row)
+  for (int row = warp; row < G; row += kDecodeWarps) {
     float M = -INFINITY;
-    for (int s2 = 0; s2 < ns; ++s2) M = fmaxf(M, __ldcg(p.ws_lse + (slot0 + s2) * G + row));
-    float L = 0.f, acc = 0.f;
-    if (M != -INFINITY) {
-      for (int s2 = 0; s2 < ns; ++s2) {
-        const float sc = fast_exp2(__ldcg(p.ws_lse + (slot0 + s2) * G + row) - M);
-        L += sc;
-        acc += sc * __ldcg(p.ws_o + (slot0 + s2) * G * D + idx);
-      }
+    for (int s2 = lane; s2 < ns; s2 += 32) M = fmaxf(M, smw[s2 * G + row]);
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
+    float L = 0.f;
+    for (int s2 = lane; s2 < ns; s2 += 32) {
+      const float w = (M == -INFINITY) ? 0.f : fast_exp2(smw[s2 * G + row] - M);
+      smw[s2 * G + row] = w;
+      L += w;
     }
-    const int64_t orow = (int64_t)sidx * p.h_q + (int64_t)kvh * G + row;
-    p.o[orow * D + dd] = (L > 0.f) ? acc / L : 0.f;
-    if (dd == 0) p.lse[orow] = (L > 0.f) ? (M + __log2f(L)) * kLn2 : -INFINITY;
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
+    const float inv = (L > 0.f) ? 1.f / L : 0.f;
+    for (int s2 = lane; s2 < ns; s2 += 32) smw[s2 * G + row] *= inv;
+    if (lane == 0)
+      p.lse[(int64_t)sidx * p.h_q + (int64_t)kvh * G + row] = (L > 0.f) ? (M + __log2f(L)) * kLn2 : -INFINITY;
+  }
+  __syncthreads();
+  // outputs: independent L2 loads over the splits (8 in flight), summed in split order
+  const float *src0 = p.ws_o + slot0 * G * D;
+  for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
+    const int row = idx / D;
+    const float *src = src0 + idx;
+    float acc = 0.f;
+    int s2 = 0;
+    for (; s2 + 8 <= ns; s2 += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (int64_t)(s2 + u) * G * D);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fmaf(smw[(s2 + u) * G + row], v[u], acc);
+    }
+    for (; s2 < ns; ++s2) acc = fmaf(smw[s2 * G + row], __ldcg(src + (int64_t)s2 * G * D), acc);
+    p.o[((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D + idx] = acc;
   }
   if (tid == 0) *ctr = 0u;  // leave the counter zeroed for the next call
 }

@@ -177,7 +177,7 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
     int cta = 0;
     for (int i = 0; i < nb; ++i) {
       const medha_kv_shard &kv = kvs[b0 + i];
-      int64_t ns = std::max<int64_t>(1, cdiv(nvis[i], per_cta));
+      int64_t ns = std::min<int64_t>(kDecodeMaxSplits, std::max<int64_t>(1, cdiv(nvis[i], per_cta)));
       int64_t split_tokens = std::max<int64_t>(64, (int64_t)round_up((size_t)cdiv(std::max<int64_t>(nvis[i], 1), ns), 64));
       ns = std::max<int64_t>(1, cdiv(nvis[i], split_tokens));
       if (split_tokens > INT32_MAX) return fail(MEDHA_ERANGE, "split too large");
