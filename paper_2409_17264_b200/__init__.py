@@ -24,6 +24,8 @@ __all__ = ["lib", "MedhaError", "KVShard", "kv_append", "attn_decode_partial", "
            "hbm_read_probe", "decode_workspace", "prefill_workspace", "kvp_workspace", "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmedha_attn.so")
+if os.environ.get("MEDHA_LIB_PATH"):          # experiment variants built by build.py --out=...
+    LIB_PATH = os.environ["MEDHA_LIB_PATH"]
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libmedha_attn.so not built at {LIB_PATH}; run `python -m paper_2409_17264_b200.build` "
                       "(there is no CPU fallback)")

@@ -45,14 +45,18 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> str:
-    if not force and up_to_date():
+def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False, out: str = None,
+          defines=()) -> str:
+    """Build the library (default: in-tree LIB).  `out`/`defines` build an experiment
+    variant elsewhere (e.g. build/variant.so with -DMEDHA_...); the product is LIB."""
+    lib_path = out or LIB
+    if not force and out is None and up_to_date():
         return LIB
     inc, lib = nccl_dirs()
     cmd = [NVCC, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-fvisibility=default", "--expt-relaxed-constexpr",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
-           *sources(), "-o", LIB + ".tmp",
+           *[f"-D{d}" for d in defines], *sources(), "-o", lib_path + ".tmp",
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
     if ptxas_v:
         cmd[1:1] = ["-Xptxas", "-v"]
@@ -64,10 +68,18 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
         raise RuntimeError("nvcc failed building libmedha_attn.so")
     if verbose or ptxas_v:
         sys.stderr.write(r.stdout + r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib_path + ".tmp", lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force=True, ptxas_v="--ptxas" in sys.argv)
-    print(LIB)
+    args = sys.argv[1:]
+    out = None
+    defs = []
+    for a in args:
+        if a.startswith("--out="):
+            out = os.path.abspath(a[6:])
+            os.makedirs(os.path.dirname(out), exist_ok=True)
+        elif a.startswith("-D"):
+            defs.append(a[2:])
+    print(build(verbose="--verbose" in args, force=True, ptxas_v="--ptxas" in args, out=out, defines=defs))

@@ -36,6 +36,9 @@ constexpr int kWsTileM = 128;
 constexpr int kWsTileN = 128;
 constexpr int kWsSlots = 4;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef MEDHA_PF_POLY_MASK
+#define MEDHA_PF_POLY_MASK 0x0  // 32-column chunks q (bit q) whose exp2 runs on the FMA pipe (A/B: off is faster)
+#endif
 
 struct PrefillWsParams {
   float *o;        // [c][h_q][D] (n_split == 1) or ws parts [n_split][part_stride]
@@ -64,6 +67,79 @@ struct WsLayout {
   static constexpr uint32_t kTotal = kBar + 256;
   static constexpr uint32_t kAlloc = kTotal + 1024;
 };
+
+// exp2 on the FMA pipe (FA4-style offload of the MUFU pipe): 2^x = 2^j * p(f), j = rint(x),
+// f = x - j in [-0.5, 0.5], p the degree-3 minimax polynomial of 2^f (max relative error
+// 7.5e-5, < 1/25 of a bf16 half-ulp).  x is clamped at -126 (2^-126 ~ 0 for P).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;            // 1.5 * 2^23: rint(x) in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  const float pf = fmaf(fmaf(fmaf(0.055171651f, f, 0.24261107f), f, 0.69326099f), f, 0.99992808f);
+  // (bits(t) << 23) == rint(x) << 23 mod 2^32 because 0x4B400000 << 23 == 0 mod 2^32
+  return __int_as_float(__float_as_int(pf) + __float_as_int(t) * 8388608);
+}
+
+// Softmax of one 128-column S row (this thread's TMEM lane), register resident: the row
+// is read from TMEM once (4 x tcgen05.ld, one wait), the max and the exponentials work on
+// registers, and P goes back as bf16 into TMEM columns [0, 64) (aliasing consumed S).
+__device__ __forceinline__ void sm_load_row(uint32_t tS, uint32_t (&s)[128]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) tmem_ld32(tS + 32 * q, reinterpret_cast<uint32_t(&)[32]>(s[32 * q]));
+  tmem_wait_ld();
+}
+
+// max of the raw logits; kMasked: only columns < nvalid count (causal diagonal / shard end)
+template <bool kMasked>
+__device__ __forceinline__ float sm_rowmax(const uint32_t (&s)[128], int nvalid) {
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < 128; e += 2) {
+    if (kMasked) {
+      if (e < nvalid) m0 = fmaxf(m0, __uint_as_float(s[e]));
+      if (e + 1 < nvalid) m1 = fmaxf(m1, __uint_as_float(s[e + 1]));
+    } else {
+      m0 = fmaxf(m0, __uint_as_float(s[e]));
+      m1 = fmaxf(m1, __uint_as_float(s[e + 1]));
+    }
+  }
+  return fmaxf(m0, m1);
+}
+
+// P = 2^(s*scale_log2 - mu) -> bf16 -> TMEM.  Returns the row sum of the bf16-ROUNDED P
+// (the exact weights the PV MMA uses).  In unmasked tiles the 32-column chunks selected by
+// MEDHA_PF_POLY_MASK evaluate exp2 with ex2_poly on the FMA pipe, the rest on MUFU.EX2.
+template <bool kMasked>
+__device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[128], float sl2, float mu,
+                                             int nvalid) {
+  float lsum0 = 0.f, lsum1 = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      const int col = 32 * q + e;
+      const float x0 = fmaf(__uint_as_float(s[col]), sl2, -mu);
+      const float x1 = fmaf(__uint_as_float(s[col + 1]), sl2, -mu);
+      float p0, p1;
+      if (!kMasked && ((MEDHA_PF_POLY_MASK >> q) & 1)) {
+        p0 = ex2_poly(x0);
+        p1 = ex2_poly(x1);
+      } else {
+        p0 = fast_exp2(x0);
+        p1 = fast_exp2(x1);
+      }
+      if (kMasked) {
+        p0 = (col < nvalid) ? p0 : 0.f;
+        p1 = (col + 1 < nvalid) ? p1 : 0.f;
+      }
+      pk[e >> 1] = pack_bf16x2(p0, p1);
+      if (e & 2) lsum1 += bf16x2_sum(pk[e >> 1]); else lsum0 += bf16x2_sum(pk[e >> 1]);
+    }
+    tmem_st16(tS + 16 * q, pk);
+  }
+  return lsum0 + lsum1;
+}
 
 template <int D, int G>
 __global__ void __launch_bounds__(kWsThreads, 1)
@@ -223,26 +299,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       tc_fence_after();
       const int64_t jb = (int64_t)(jt0 + j) * kWsTileN;
       const bool full = (jb + kWsTileN - 1) <= j_lim_tile;
-      const int nvalid = full ? kWsTileN : (int)min64(kWsTileN, max64(0, j_lim - jb + 1));
-      // ---- pass 1: row max -------------------------------------------------------
-      float mx = -INFINITY;
-#pragma unroll
-      for (int q2 = 0; q2 < 4; q2 += 2) {
-        uint32_t ra[32], rb[32];
-        tmem_ld32(tS + 32 * q2, ra);
-        tmem_ld32(tS + 32 * (q2 + 1), rb);
-        tmem_wait_ld();
-        if (full) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, fmaxf(__uint_as_float(ra[e]), __uint_as_float(rb[e])));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            if (32 * q2 + e < nvalid) mx = fmaxf(mx, __uint_as_float(ra[e]));
-            if (32 * (q2 + 1) + e < nvalid) mx = fmaxf(mx, __uint_as_float(rb[e]));
-          }
-        }
-      }
+      const int nvalid = (int)min64(kWsTileN, max64(0, j_lim - jb + 1));   // valid cols [0, nvalid)
+      // ---- row max (unmasked tiles take a compare-free path) ---------------------------
+      uint32_t sreg[128];
+      sm_load_row(tS, sreg);
+      const float mx = full ? sm_rowmax<false>(sreg, nvalid) : sm_rowmax<true>(sreg, nvalid);
       const float m_tile = ceilf(mx * sl2);   // integer-valued (log2 units): exact rescales
       float m_use = m_run, alpha = 1.f;
       bool rescale = false;
@@ -253,6 +314,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       }
       m_run = m_use;
       const float mu = (m_use == -INFINITY) ? 0.f : m_use;
+      // ---- P = exp2(s*scale - m) -> bf16 -> TMEM (aliasing S) ------------------------
+      const float lsum = full ? sm_exp_pack<false>(tS, sreg, sl2, mu, nvalid)
+                              : sm_exp_pack<true>(tS, sreg, sl2, mu, nvalid);
       // ---- O rescale (PV_X(j-1) is complete: covered by the S_X(j) commit) ----------
       if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll
@@ -264,27 +328,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           for (int e = 0; e < 32; ++e) ro[e] = __float_as_uint(__uint_as_float(ro[e]) * alpha);
           tmem_st32(tO + 32 * q, ro);
         }
-      }
-      // ---- pass 2: P = exp2(s*scale - m) -> bf16 -> TMEM (aliasing S) ------------
-      float lsum = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t ra[32];
-        tmem_ld32(tS + 32 * q, ra);
-        tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float p0 = fast_exp2(fmaf(__uint_as_float(ra[e]), sl2, -mu));
-          float p1 = fast_exp2(fmaf(__uint_as_float(ra[e + 1]), sl2, -mu));
-          if (!full) {
-            p0 = (32 * q + e < nvalid) ? p0 : 0.f;
-            p1 = (32 * q + e + 1 < nvalid) ? p1 : 0.f;
-          }
-          pk[e >> 1] = pack_bf16x2(p0, p1);
-          lsum += bf16x2_sum(pk[e >> 1]);   // normaliser of the rounded P (consistent weights)
-        }
-        tmem_st16(tS + 16 * q, pk);
       }
       l_run = l_run * alpha + lsum;
       tmem_wait_st();
