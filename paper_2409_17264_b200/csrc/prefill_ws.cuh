@@ -36,8 +36,14 @@ constexpr int kWsTileM = 128;
 constexpr int kWsTileN = 128;
 constexpr int kWsSlots = 4;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-#ifndef MEDHA_PF_POLY_MASK
-#define MEDHA_PF_POLY_MASK 0x0  // 32-column chunks q (bit q) whose exp2 runs on the FMA pipe (A/B: off is faster)
+#ifndef MEDHA_PF_SETMAXNREG
+#define MEDHA_PF_SETMAXNREG 0   // rebalance registers between warpgroups (A/B knob)
+#endif
+#ifndef MEDHA_PF_POLY_NUM      // fraction NUM/DEN of column pairs whose exp2 runs on the FMA pipe
+#define MEDHA_PF_POLY_NUM 0
+#endif
+#ifndef MEDHA_PF_POLY_DEN
+#define MEDHA_PF_POLY_DEN 3
 #endif
 
 struct PrefillWsParams {
@@ -106,39 +112,54 @@ __device__ __forceinline__ float sm_rowmax(const uint32_t (&s)[128], int nvalid)
   return fmaxf(m0, m1);
 }
 
+// Packed (fp32x2) version of ex2_poly: FADD2/FFMA2 on the FMA pipe, IMAD for the
+// exponent, FMNMX for the clamp - no MUFU.  Same polynomial and error as ex2_poly.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
+  float2 pf = __ffma2_rn(make_float2(0.055171651f, 0.055171651f), f, make_float2(0.24261107f, 0.24261107f));
+  pf = __ffma2_rn(pf, f, make_float2(0.69326099f, 0.69326099f));
+  pf = __ffma2_rn(pf, f, make_float2(0.99992808f, 0.99992808f));
+  return make_float2(__int_as_float(__float_as_int(pf.x) + __float_as_int(t.x) * 8388608),
+                     __int_as_float(__float_as_int(pf.y) + __float_as_int(t.y) * 8388608));
+}
+
 // P = 2^(s*scale_log2 - mu) -> bf16 -> TMEM.  Returns the row sum of the bf16-ROUNDED P
-// (the exact weights the PV MMA uses).  In unmasked tiles the 32-column chunks selected by
-// MEDHA_PF_POLY_MASK evaluate exp2 with ex2_poly on the FMA pipe, the rest on MUFU.EX2.
+// (the exact weights the PV MMA uses).  In unmasked tiles, column pairs i with
+// (i % MEDHA_PF_POLY_DEN) < MEDHA_PF_POLY_NUM evaluate exp2 with ex2_poly2 on the FMA pipe
+// (offloading the MUFU pipe, the softmax bottleneck: 128 ex2 per row per tile), the rest
+// with MUFU.EX2.
 template <bool kMasked>
 __device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[128], float sl2, float mu,
                                              int nvalid) {
-  float lsum0 = 0.f, lsum1 = 0.f;
+  float2 lsum2 = make_float2(0.f, 0.f);
+  const float2 sl2v = make_float2(sl2, sl2), nmu = make_float2(-mu, -mu);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t pk[16];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
       const int col = 32 * q + e;
-      const float x0 = fmaf(__uint_as_float(s[col]), sl2, -mu);
-      const float x1 = fmaf(__uint_as_float(s[col + 1]), sl2, -mu);
-      float p0, p1;
-      if (!kMasked && ((MEDHA_PF_POLY_MASK >> q) & 1)) {
-        p0 = ex2_poly(x0);
-        p1 = ex2_poly(x1);
+      const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[col]), __uint_as_float(s[col + 1])), sl2v, nmu);
+      float2 pp;
+      if (!kMasked && ((col >> 1) % MEDHA_PF_POLY_DEN) < MEDHA_PF_POLY_NUM) {
+        pp = ex2_poly2(x);
       } else {
-        p0 = fast_exp2(x0);
-        p1 = fast_exp2(x1);
+        pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
       }
       if (kMasked) {
-        p0 = (col < nvalid) ? p0 : 0.f;
-        p1 = (col + 1 < nvalid) ? p1 : 0.f;
+        pp.x = (col < nvalid) ? pp.x : 0.f;
+        pp.y = (col + 1 < nvalid) ? pp.y : 0.f;
       }
-      pk[e >> 1] = pack_bf16x2(p0, p1);
-      if (e & 2) lsum1 += bf16x2_sum(pk[e >> 1]); else lsum0 += bf16x2_sum(pk[e >> 1]);
+      pk[e >> 1] = pack_bf16x2(pp.x, pp.y);
+      lsum2 = __fadd2_rn(lsum2, make_float2(__uint_as_float(pk[e >> 1] << 16), __uint_as_float(pk[e >> 1] & 0xffff0000u)));
     }
     tmem_st16(tS + 16 * q, pk);
   }
-  return lsum0 + lsum1;
+  return lsum2.x + lsum2.y;
 }
 
 template <int D, int G>
@@ -193,6 +214,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#if MEDHA_PF_SETMAXNREG
+  // rebalance the register file: producer/MMA warpgroup shrinks, softmax warpgroups grow
+  if (warp < 4)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+  else
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+#endif
 
   uint8_t *sQ = smem + L::kQ0;
   auto slot_ptr = [&](int s) { return smem + L::kSlot0 + s * L::kSlotBytes; };
