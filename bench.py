@@ -161,6 +161,9 @@ def bench_decode(args, rank, world, M):
     o_out = torch.empty((1, H_Q, D), dtype=torch.float32, device="cuda")
     lse_out = torch.empty((1, H_Q), dtype=torch.float32, device="cuda")
     xws = M.exchange_workspace(world, rows, D) if world > 1 else None
+    kws = M.kvp_workspace(world, 1, H_Q, H_KV, D) if world > 1 else None
+    if comm is not None and os.environ.get("MEDHA_BENCH_NCCL") == "1":
+        comm.set_p2p(False)                       # A/B: NCCL all-gather + merge kernel
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
 
     def step(i=None):
@@ -172,6 +175,11 @@ def bench_decode(args, rank, world, M):
             e[0].record(stream)
         if world == 1:
             M.attn_decode_partial([sh], q, [new_pos], o=o_out, lse=lse_out, ws=dws)
+            if e:
+                e[1].record(stream)
+        elif comm.p2p:
+            # one launch: decode partial + NVLink push + rank-ordered merge (fused exchange)
+            M.kvp_decode(comm, [sh], q, [new_pos], ws=kws, o=o_out, lse=lse_out)
             if e:
                 e[1].record(stream)
         else:
@@ -236,10 +244,12 @@ def bench_decode(args, rank, world, M):
     bytes_rank = acc.decode_bytes(sh.len, H_KV, D)
     h2d = world * (H_Q * D * 2) + 2 * H_KV * D * 2
     d2h = world * (H_Q * D * 4 + H_Q * 4)
-    launches_per_step = (2 if tail else 1) + (1 if world > 1 else 0)   # rank-0 view
+    fused = comm is not None and comm.p2p
+    launches_per_step = (2 if tail else 1) + (1 if (world > 1 and not fused) else 0)   # rank-0 view
+    exch = "none" if comm is None else ("fused NVLink push in the decode kernel" if fused else "NCCL all-gather + merge kernel")
     if comm is not None:
         comm.close()
-    return dict(ms=ms, kern_ms=kern_ms, bytes_total=bytes_total, bytes_rank=bytes_rank, e2e_ms=e2e_ms,
+    return dict(exchange=exch, ms=ms, kern_ms=kern_ms, bytes_total=bytes_total, bytes_rank=bytes_rank, e2e_ms=e2e_ms,
                 h2d=h2d, d2h=d2h, clocks=clk, launches=launches_per_step * args.steps, e2e_diff=e2e_diff,
                 o=o_out, sh=sh)
 
@@ -449,6 +459,7 @@ def main():
                     "ms_per_step": round(r["e2e_ms"], 5), "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
                     "api": "medha_decode_step_host", "max_abs_vs_device_path": r["e2e_diff"]},
             "gpu_launches": r["launches"],
+            "kvp_exchange": r["exchange"],
             "clocks": r["clocks"],
             "cpu_baseline": cpu,
         }

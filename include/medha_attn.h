@@ -152,6 +152,19 @@ medha_status medha_kvp_comm_create(const uint8_t id[128], int32_t rank, int32_t 
                                    medha_kvp_comm **out);
 medha_status medha_kvp_comm_destroy(medha_kvp_comm *comm);
 medha_status medha_kvp_comm_info(const medha_kvp_comm *comm, int32_t *rank, int32_t *world);
+/*
+ * Fused peer-to-peer exchange (single node, NVLink).  medha_kvp_comm_create also
+ * allocates a receive buffer (~2 x world x 2.1 MB + flags) and maps every peer's buffer
+ * through CUDA IPC (a collective; skipped when MEDHA_KVP_P2P=0 or when any rank fails).
+ * When active, medha_kvp_decode (batch <= 64) runs the exchange inside the decode kernel:
+ * the last CTA of each (sequence, kv head) stores the rank partial into every rank's
+ * receive slot over NVLink, raises the peers' epoch flags (release, system scope), waits
+ * for all ranks' flags (acquire) and merges in rank order - no NCCL call, no merge launch.
+ * medha_kvp_comm_p2p returns 1 when that path is active; medha_kvp_comm_set_p2p(comm, 0)
+ * forces the NCCL all-gather + merge path (must be switched identically on all ranks).
+ */
+int32_t medha_kvp_comm_p2p(const medha_kvp_comm *comm);
+medha_status medha_kvp_comm_set_p2p(medha_kvp_comm *comm, int32_t enable);
 
 /*
  * kvp_decode (Eq. 5): the local partial (medha_attn_decode_partial on

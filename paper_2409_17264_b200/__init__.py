@@ -62,6 +62,8 @@ _sig("medha_kvp_unique_id", _i32, _vp)
 _sig("medha_kvp_comm_create", _i32, _vp, _i32, _i32, _P(_vp))
 _sig("medha_kvp_comm_destroy", _i32, _vp)
 _sig("medha_kvp_comm_info", _i32, _vp, _P(_i32), _P(_i32))
+_sig("medha_kvp_comm_p2p", _i32, _vp)
+_sig("medha_kvp_comm_set_p2p", _i32, _vp, _i32)
 _sig("medha_kvp_workspace_size", _sz, _i32, _i32, _i32, _i32, _i32)
 _sig("medha_kvp_decode", _i32, _vp, _P(_Shard), _i32, _vp, _i32, _P(_i64), _f32, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("medha_kvp_exchange_workspace_size", _sz, _i32, _i64, _i32)
@@ -245,6 +247,16 @@ class KVPComm:
         _check(lib.medha_kvp_comm_create(uid, self.rank, self.world, ctypes.byref(h)), "kvp_comm_create")
         self.handle = h
 
+    @property
+    def p2p(self) -> bool:
+        """True when kvp_decode runs the fused NVLink exchange inside the decode kernel."""
+        return bool(lib.medha_kvp_comm_p2p(self.handle))
+
+    def set_p2p(self, enable: bool) -> None:
+        """Switch between the fused NVLink exchange and NCCL all-gather + merge (collective:
+        call identically on every rank)."""
+        _check(lib.medha_kvp_comm_set_p2p(self.handle, int(bool(enable))), "kvp_comm_set_p2p")
+
     def close(self):
         if self.handle:
             _check(lib.medha_kvp_comm_destroy(self.handle), "kvp_comm_destroy")
@@ -258,12 +270,16 @@ class KVPComm:
 
 
 def kvp_decode(comm: KVPComm, shards: Sequence[KVShard], q: torch.Tensor, q_pos: Sequence[int], scale=None,
-               want_bf16=False, ws=None, stream=None):
-    """Eq. 5: local partial + NCCL all-gather + rank-ordered LSE merge; identical on all ranks."""
+               want_bf16=False, ws=None, stream=None, o=None, lse=None):
+    """Eq. 5: local partial + exchange (fused NVLink push inside the decode kernel when
+    comm.p2p, else NCCL all-gather + merge kernel) + rank-ordered LSE merge; identical on
+    all ranks."""
     _need_cuda(q, "q", torch.bfloat16)
     B, h_q, d = q.shape
-    o = torch.empty((B, h_q, d), dtype=torch.float32, device=q.device)
-    lse = torch.empty((B, h_q), dtype=torch.float32, device=q.device)
+    if o is None:
+        o = torch.empty((B, h_q, d), dtype=torch.float32, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, h_q), dtype=torch.float32, device=q.device)
     ob = torch.empty((B, h_q, d), dtype=torch.bfloat16, device=q.device) if want_bf16 else None
     if ws is None:
         ws = kvp_workspace(comm.world, B, h_q, shards[0].h_kv, d, q.device)

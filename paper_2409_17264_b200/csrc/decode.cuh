@@ -28,7 +28,24 @@
 
 namespace medha {
 
+#ifdef MEDHA_DECODE_TRACE
+// experiment-only instrumentation: %globaltimer per CTA at start / main-loop end / partial
+// written / split merge done (read back with medha_debug_decode_trace)
+__device__ unsigned long long g_decode_trace[8192][8];
+#define MEDHA_TRACE(k)                                                                     \
+  do {                                                                                     \
+    if (threadIdx.x == 0 && blockIdx.x < 8192) {                                           \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+      g_decode_trace[blockIdx.x][k] = t_;                                                  \
+    }                                                                                      \
+  } while (0)
+#else
+#define MEDHA_TRACE(k) do {} while (0)
+#endif
+
 constexpr int kDecodeMaxSeqPerLaunch = 64;
+constexpr int kMaxKvpRanks = 8;
 constexpr int kDecodeMaxSplits = 256;  // per (seq, kv head): the merge weights live in sm_o
 constexpr int kDecodeWarps = 4;
 constexpr int kDecodeThreads = kDecodeWarps * 32;
@@ -55,8 +72,35 @@ struct DecodeParams {
   int32_t n_seq;
   int32_t h_kv;
   int32_t h_q;
+  // ---- fused KVP exchange over NVLink.  x_world == 0: off. ----
+  // The last CTA of every (seq, kv head) pushes the unit's rank partial into every rank's
+  // receive slot (peer memory mapped with CUDA IPC), raises that rank's flag for the unit
+  // to `x_epoch` (release, system scope), waits for the flags of all ranks (acquire) and
+  // merges the world's partials in rank order into x_o / x_lse / x_obf.
+  int32_t x_world;
+  int32_t x_rank;
+  uint32_t x_epoch;
+  int32_t x_units;                 // flag stride per source rank
+  int64_t x_rows;                  // rows of the packed slot layout: o [x_rows][D], lse [x_rows]
+  int64_t x_slot;                  // floats per source-rank slot
+  float *x_dst[kMaxKvpRanks];      // rank r's receive slot for THIS rank (parity resolved)
+  uint32_t *x_flag_dst[kMaxKvpRanks];  // rank r's flags for THIS rank: [x_units]
+  const float *x_recv;             // local receive slots: [x_world][x_slot]
+  const uint32_t *x_flags;         // local flags: [x_world][x_units]
+  float *x_o;                      // final outputs [rows][D]
+  float *x_lse;                    // final lse [rows] (may be null)
+  __nv_bfloat16 *x_obf;            // final bf16 outputs (may be null)
   DecodeSeq seq[kDecodeMaxSeqPerLaunch];
 };
+
+__device__ __forceinline__ void st_release_sys(uint32_t *ptr, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *ptr) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
 
 template <int D, int G>
 __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const __grid_constant__ DecodeParams p) {
@@ -132,6 +176,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     }
   };
 
+  MEDHA_TRACE(0);
   int64_t tb = t_begin + 16 * warp;
   if (tb < t_end) load_tile(tb, kr, vr);
   for (; tb < t_end; tb += 16 * kDecodeWarps) {
@@ -232,6 +277,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     }
   }
 
+  MEDHA_TRACE(1);
   // ---- per-warp reduction of l over the 4 lanes of a row, publish to smem --------------
   l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
   l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
@@ -282,6 +328,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
         p.ws_lse[slot * G + row] = lse2;
     }
   }
+  MEDHA_TRACE(2);
   if (single) return;
 
   // ---- last CTA of this (seq, kv head) merges the splits in split order -----------------
@@ -313,28 +360,105 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
     const float inv = (L > 0.f) ? 1.f / L : 0.f;
     for (int s2 = lane; s2 < ns; s2 += 32) smw[s2 * G + row] *= inv;
-    if (lane == 0)
-      p.lse[(int64_t)sidx * p.h_q + (int64_t)kvh * G + row] = (L > 0.f) ? (M + __log2f(L)) * kLn2 : -INFINITY;
+    if (lane == 0) {
+      const float lse_r = (L > 0.f) ? (M + __log2f(L)) * kLn2 : -INFINITY;
+      const int64_t orow = (int64_t)sidx * p.h_q + (int64_t)kvh * G + row;
+      if (p.x_world > 0) {
+        for (int r = 0; r < p.x_world; ++r) p.x_dst[r][p.x_rows * D + orow] = lse_r;   // NVLink stores
+      } else {
+        p.lse[orow] = lse_r;
+      }
+    }
   }
   __syncthreads();
-  // outputs: independent L2 loads over the splits (8 in flight), summed in split order
-  const float *src0 = p.ws_o + slot0 * G * D;
-  for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
-    const int row = idx / D;
-    const float *src = src0 + idx;
-    float acc = 0.f;
-    int s2 = 0;
-    for (; s2 + 8 <= ns; s2 += 8) {
-      float v[8];
+  // outputs: every thread owns OPT outputs and streams the splits in batches of SB, so
+  // OPT*SB independent L2 loads are in flight (the merge sits on the kernel's critical
+  // path: one latency round per batch); summed in split order (deterministic).
+  constexpr int OPT = (G * D + kDecodeThreads - 1) / kDecodeThreads;   // 1..16 outputs per thread
+  const bool own0 = tid < G * D;                                        // (G*D = 64 for G=1, D=64)
+  constexpr int SB = OPT >= 8 ? 4 : 8;
+  const float *src0 = p.ws_o + slot0 * G * D + tid;
+  float acc[OPT];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (int64_t)(s2 + u) * G * D);
+  for (int i = 0; i < OPT; ++i) acc[i] = 0.f;
+  for (int s2 = 0; s2 < ns; s2 += SB) {
+    float v[SB][OPT];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc = fmaf(smw[(s2 + u) * G + row], v[u], acc);
-    }
-    for (; s2 < ns; ++s2) acc = fmaf(smw[s2 * G + row], __ldcg(src + (int64_t)s2 * G * D), acc);
-    p.o[((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D + idx] = acc;
+    for (int u = 0; u < SB; ++u)
+#pragma unroll
+      for (int i = 0; i < OPT; ++i)
+        v[u][i] = (s2 + u < ns && own0) ? __ldcg(src0 + (int64_t)(s2 + u) * G * D + i * kDecodeThreads) : 0.f;
+#pragma unroll
+    for (int u = 0; u < SB; ++u)
+#pragma unroll
+      for (int i = 0; i < OPT; ++i)
+        if (s2 + u < ns && own0) acc[i] = fmaf(smw[(s2 + u) * G + (tid + i * kDecodeThreads) / D], v[u][i], acc[i]);
   }
+  const int64_t obase = ((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D + tid;
   if (tid == 0) *ctr = 0u;  // leave the counter zeroed for the next call
+  if (p.x_world == 0) {
+#pragma unroll
+    for (int i = 0; i < OPT; ++i)
+      if (own0) p.o[obase + i * kDecodeThreads] = acc[i];
+    MEDHA_TRACE(3);
+    return;
+  }
+  // ---- fused KVP exchange: push this unit's partial to every rank, then merge ----------
+  for (int r = 0; r < p.x_world; ++r) {
+#pragma unroll
+    for (int i = 0; i < OPT; ++i)
+      if (own0) p.x_dst[r][obase + i * kDecodeThreads] = acc[i];                 // NVLink stores
+  }
+  MEDHA_TRACE(4);
+  __syncthreads();
+  // one system-scope fence after the barrier orders every thread's NVLink stores before
+  // the flag stores (cumulativity through bar.sync)
+  if (tid == 0) __threadfence_system();
+  __syncthreads();
+  MEDHA_TRACE(5);
+  const int unit = sidx * p.h_kv + kvh;
+  if (tid < p.x_world) {
+    st_release_sys(p.x_flag_dst[tid] + unit, p.x_epoch);
+    const uint32_t *f = p.x_flags + (int64_t)tid * p.x_units + unit;
+    while (ld_acquire_sys(f) != p.x_epoch) {
+    }
+  }
+  __syncthreads();
+  MEDHA_TRACE(6);
+  // merge in rank order (same formula and order as lse_merge_kernel): identical on all ranks
+  float *xw = smw;                                  // [x_world][G] weights
+  const int64_t lrow0 = p.x_rows * D + (int64_t)sidx * p.h_q + (int64_t)kvh * G;
+  if (tid < G) {
+    const int row = tid;
+    float M = -INFINITY;
+    for (int r = 0; r < p.x_world; ++r) M = fmaxf(M, __ldcg(p.x_recv + (int64_t)r * p.x_slot + lrow0 + row));
+    float lse_f = -INFINITY;
+    if (M != -INFINITY) {
+      float ssum = 0.f;
+      for (int r = 0; r < p.x_world; ++r) ssum += __expf(__ldcg(p.x_recv + (int64_t)r * p.x_slot + lrow0 + row) - M);
+      lse_f = M + __logf(ssum);
+    }
+    for (int r = 0; r < p.x_world; ++r)
+      xw[r * G + row] = (M == -INFINITY) ? 0.f : __expf(__ldcg(p.x_recv + (int64_t)r * p.x_slot + lrow0 + row) - lse_f);
+    if (p.x_lse) p.x_lse[(int64_t)sidx * p.h_q + (int64_t)kvh * G + row] = lse_f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < OPT; ++i) {
+    if (!own0) break;
+    const int row = (tid + i * kDecodeThreads) / D;
+    float v[kMaxKvpRanks];
+#pragma unroll
+    for (int r = 0; r < kMaxKvpRanks; ++r)
+      v[r] = (r < p.x_world) ? __ldcg(p.x_recv + (int64_t)r * p.x_slot + obase + i * kDecodeThreads) : 0.f;
+    float o = 0.f;
+#pragma unroll
+    for (int r = 0; r < kMaxKvpRanks; ++r)
+      if (r < p.x_world) o += xw[r * G + row] * v[r];
+    p.x_o[obase + i * kDecodeThreads] = o;
+    if (p.x_obf) p.x_obf[obase + i * kDecodeThreads] = __float2bfloat16_rn(o);
+  }
+  MEDHA_TRACE(3);
 }
 
 }  // namespace medha

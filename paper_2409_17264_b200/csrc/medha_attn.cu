@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -46,6 +47,11 @@ medha_status fail(medha_status s, const char *fmt, ...) {
     cudaError_t e_ = cudaGetLastError();                                                        \
     if (e_ != cudaSuccess) return fail(MEDHA_ECUDA, "%s launch: %s", what, cudaGetErrorString(e_)); \
   } while (0)
+
+int getenv_flag(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -128,9 +134,22 @@ medha_status dispatch_decode_g(int G, const DecodeParams &p, int grid, cudaStrea
   return MEDHA_OK;
 }
 
+// Fused-exchange settings of one decode launch (see DecodeParams::x_*); null = off.
+struct DecodeXchg {
+  int32_t world, rank, units;
+  uint32_t epoch;
+  int64_t rows, slot;
+  float *dst[kMaxKvpRanks];
+  uint32_t *flag_dst[kMaxKvpRanks];
+  const float *recv;
+  const uint32_t *flags;
+  float *o, *lse;
+  __nv_bfloat16 *obf;
+};
+
 medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const void *q, int32_t h_q,
                                  const int64_t *q_pos, float scale, float *o, float *lse, void *ws,
-                                 size_t ws_bytes, cudaStream_t st) {
+                                 size_t ws_bytes, cudaStream_t st, const DecodeXchg *x = nullptr) {
   if (batch < 0) return fail(MEDHA_EINVAL, "negative batch");
   if (batch == 0) return MEDHA_OK;
   if (!kvs || !q || !q_pos || !o || !lse) return fail(MEDHA_EINVAL, "null argument");
@@ -151,6 +170,7 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
   decode_ws_layout(batch, h_q, h_kv, d, static_cast<char *>(ws), &W);
   if (ws_bytes < W.bytes) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, W.bytes);
 
+  if (x && batch > kDecodeMaxSeqPerLaunch) return fail(MEDHA_ENOTSUP, "fused exchange needs batch <= 64");
   const int target = 2 * num_sms();  // two 4-warp CTAs per SM
   for (int b0 = 0; b0 < batch; b0 += kDecodeMaxSeqPerLaunch) {
     const int nb = std::min(kDecodeMaxSeqPerLaunch, batch - b0);
@@ -166,6 +186,23 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
     p.n_seq = nb;
     p.h_kv = h_kv;
     p.h_q = h_q;
+    if (x) {
+      p.x_world = x->world;
+      p.x_rank = x->rank;
+      p.x_epoch = x->epoch;
+      p.x_units = x->units;
+      p.x_rows = x->rows;
+      p.x_slot = x->slot;
+      for (int r = 0; r < x->world; ++r) {
+        p.x_dst[r] = x->dst[r];
+        p.x_flag_dst[r] = x->flag_dst[r];
+      }
+      p.x_recv = x->recv;
+      p.x_flags = x->flags;
+      p.x_o = x->o;
+      p.x_lse = x->lse;
+      p.x_obf = x->obf;
+    }
     int64_t total = 0;
     std::vector<int64_t> nvis(nb);
     for (int i = 0; i < nb; ++i) {
@@ -180,6 +217,7 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
       int64_t ns = std::min<int64_t>(kDecodeMaxSplits, std::max<int64_t>(1, cdiv(nvis[i], per_cta)));
       int64_t split_tokens = std::max<int64_t>(64, (int64_t)round_up((size_t)cdiv(std::max<int64_t>(nvis[i], 1), ns), 64));
       ns = std::max<int64_t>(1, cdiv(nvis[i], split_tokens));
+      if (x && ns < 2) ns = 2;  // the exchange runs in the split-merging last CTA
       if (split_tokens > INT32_MAX) return fail(MEDHA_ERANGE, "split too large");
       DecodeSeq &S = p.seq[i];
       S.k = static_cast<const __nv_bfloat16 *>(kv.k);
@@ -382,7 +420,102 @@ medha_status prefill_impl(const medha_kv_shard *kv, const void *q, int64_t c, in
 struct medha_kvp_comm {
   ncclComm_t nccl;
   int32_t rank, world;
+  // fused P2P exchange (single node, CUDA IPC): one buffer per rank holding
+  // [2 parities][world src][slot floats] receive slots + [2][world][units] epoch flags
+  bool p2p = false;
+  bool p2p_on = false;      // runtime switch (medha_kvp_comm_set_p2p)
+  int device = -1;
+  char *local = nullptr;    // this rank's buffer
+  char *peer[kMaxKvpRanks] = {};  // every rank's buffer mapped here (peer[rank] = local)
+  int64_t slot = 0;         // floats per (parity, src) slot
+  int32_t units = 0;        // flags per (parity, src)
+  uint32_t epoch = 0;
 };
+
+namespace {
+constexpr int64_t kP2PSlotFloats = (int64_t)64 * 64 * 129;   // batch 64 x h_q 64 x (d 128 + 1)
+constexpr int32_t kP2PUnits = 4096;                           // (seq, kv head) units per call
+
+size_t p2p_bytes(int world) {
+  return (size_t)2 * world * kP2PSlotFloats * sizeof(float) + (size_t)2 * world * kP2PUnits * sizeof(uint32_t);
+}
+float *p2p_slot(const medha_kvp_comm *c, char *base, int parity, int src) {
+  return reinterpret_cast<float *>(base) + ((int64_t)parity * c->world + src) * c->slot;
+}
+uint32_t *p2p_flags(const medha_kvp_comm *c, char *base, int parity, int src) {
+  return reinterpret_cast<uint32_t *>(base + (size_t)2 * c->world * c->slot * sizeof(float)) +
+         ((int64_t)parity * c->world + src) * c->units;
+}
+
+// Collective: allocate the receive buffer, exchange CUDA IPC handles with ncclAllGather
+// and map every peer's buffer.  Any failure leaves the communicator on the NCCL path.
+void p2p_setup(medha_kvp_comm *c) {
+  if (c->world < 2 || c->world > kMaxKvpRanks || getenv_flag("MEDHA_KVP_P2P", 1) == 0) return;
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return;
+  const size_t bytes = p2p_bytes(c->world);
+  cudaIpcMemHandle_t *hs = nullptr;
+  cudaIpcMemHandle_t mine;
+  int ok = 1;
+  void *dbuf = nullptr;
+  int *dok = nullptr;
+  if (cudaMalloc(&c->local, bytes) != cudaSuccess || cudaMemset(c->local, 0, bytes) != cudaSuccess ||
+      cudaIpcGetMemHandle(&mine, c->local) != cudaSuccess)
+    ok = 0;
+  // agree on success everywhere (a partial setup would deadlock the fused kernels)
+  if (cudaMalloc(&dbuf, sizeof(cudaIpcMemHandle_t) * (c->world + 1)) != cudaSuccess) ok = 0;
+  if (cudaMalloc(&dok, sizeof(int)) != cudaSuccess) {
+    cudaFree(dbuf);
+    cudaStreamDestroy(st);
+    if (c->local) cudaFree(c->local);
+    c->local = nullptr;
+    return;
+  }
+  cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice);
+  ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, c->nccl, st);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost);
+  if (ok) {
+    char *slots = static_cast<char *>(dbuf);
+    cudaMemcpy(slots + sizeof(cudaIpcMemHandle_t) * c->world, &mine, sizeof(mine), cudaMemcpyHostToDevice);
+    ncclAllGather(slots + sizeof(cudaIpcMemHandle_t) * c->world, slots, sizeof(cudaIpcMemHandle_t), ncclChar,
+                  c->nccl, st);
+    cudaStreamSynchronize(st);
+    hs = new cudaIpcMemHandle_t[c->world];
+    cudaMemcpy(hs, slots, sizeof(cudaIpcMemHandle_t) * c->world, cudaMemcpyDeviceToHost);
+    for (int r = 0; r < c->world; ++r) {
+      if (r == c->rank) {
+        c->peer[r] = c->local;
+        continue;
+      }
+      void *ptr = nullptr;
+      if (cudaIpcOpenMemHandle(&ptr, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) ok = 0;
+      c->peer[r] = static_cast<char *>(ptr);
+    }
+    cudaGetLastError();
+    cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice);
+    ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, c->nccl, st);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost);
+  }
+  if (ok) {
+    c->slot = kP2PSlotFloats;
+    c->units = kP2PUnits;
+    c->p2p = c->p2p_on = true;
+  } else {
+    for (int r = 0; r < c->world; ++r)
+      if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+    if (c->local) cudaFree(c->local);
+    c->local = nullptr;
+    for (int r = 0; r < kMaxKvpRanks; ++r) c->peer[r] = nullptr;
+  }
+  delete[] hs;
+  cudaFree(dbuf);
+  cudaFree(dok);
+  cudaStreamDestroy(st);
+  cudaGetLastError();
+}
+}  // namespace
 
 extern "C" {
 
@@ -482,12 +615,20 @@ medha_status medha_kvp_comm_create(const uint8_t id[128], int32_t rank, int32_t 
     delete c;
     return fail(MEDHA_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
   }
+  cudaGetDevice(&c->device);
+  p2p_setup(c);
   *out = c;
   return MEDHA_OK;
 }
 
 medha_status medha_kvp_comm_destroy(medha_kvp_comm *comm) {
   if (!comm) return MEDHA_OK;
+  if (comm->p2p) {
+    cudaDeviceSynchronize();
+    for (int r = 0; r < comm->world; ++r)
+      if (r != comm->rank && comm->peer[r]) cudaIpcCloseMemHandle(comm->peer[r]);
+    cudaFree(comm->local);
+  }
   ncclResult_t r = ncclCommDestroy(comm->nccl);
   delete comm;
   if (r != ncclSuccess) return fail(MEDHA_ENCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
@@ -498,6 +639,15 @@ medha_status medha_kvp_comm_info(const medha_kvp_comm *comm, int32_t *rank, int3
   if (!comm) return fail(MEDHA_EINVAL, "null comm");
   if (rank) *rank = comm->rank;
   if (world) *world = comm->world;
+  return MEDHA_OK;
+}
+
+int32_t medha_kvp_comm_p2p(const medha_kvp_comm *comm) { return (comm && comm->p2p && comm->p2p_on) ? 1 : 0; }
+
+medha_status medha_kvp_comm_set_p2p(medha_kvp_comm *comm, int32_t enable) {
+  if (!comm) return fail(MEDHA_EINVAL, "null comm");
+  if (enable && !comm->p2p) return fail(MEDHA_ENOTSUP, "peer-to-peer exchange unavailable on this communicator");
+  comm->p2p_on = enable != 0;
   return MEDHA_OK;
 }
 
@@ -556,6 +706,30 @@ medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_ho
   float *send = reinterpret_cast<float *>(base);
   float *recv = reinterpret_cast<float *>(base + round_up(count * 4, 256));
   char *dws = base + kvp_buf_bytes(comm->world, rows, d);
+  if (comm->p2p && comm->p2p_on && batch <= kDecodeMaxSeqPerLaunch && (int64_t)count <= comm->slot &&
+      (int64_t)batch * h_kv <= comm->units) {
+    // fused: the decode kernel's last CTAs push the partials over NVLink and merge
+    DecodeXchg x;
+    memset(&x, 0, sizeof(x));
+    x.world = comm->world;
+    x.rank = comm->rank;
+    x.epoch = ++comm->epoch;
+    x.units = comm->units;
+    x.rows = rows;
+    x.slot = comm->slot;
+    const int par = (int)(x.epoch & 1u);
+    for (int r = 0; r < comm->world; ++r) {
+      x.dst[r] = p2p_slot(comm, comm->peer[r], par, comm->rank);
+      x.flag_dst[r] = p2p_flags(comm, comm->peer[r], par, comm->rank);
+    }
+    x.recv = p2p_slot(comm, comm->local, par, 0);
+    x.flags = p2p_flags(comm, comm->local, par, 0);
+    x.o = o_out;
+    x.lse = lse_out;
+    x.obf = static_cast<__nv_bfloat16 *>(o_out_bf16);
+    return decode_partial_impl(kvs_host, batch, q, h_q, q_pos_host, scale, o_out, send + rows * d, dws,
+                               ws_bytes - (size_t)(dws - base), st, &x);
+  }
   medha_status s = decode_partial_impl(kvs_host, batch, q, h_q, q_pos_host, scale, send, send + rows * d, dws,
                                        ws_bytes - (size_t)(dws - base), st);
   if (s) return s;
@@ -643,6 +817,13 @@ medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, in
   if (lse_host) CUDA_TRY(cudaMemcpyAsync(lse_host, lse_dev, (size_t)h_q * 4, cudaMemcpyDeviceToHost, st));
   return MEDHA_OK;
 }
+
+#ifdef MEDHA_DECODE_TRACE
+medha_status medha_debug_decode_trace(unsigned long long *host_out /* [8192][8] */) {
+  CUDA_TRY(cudaMemcpyFromSymbol(host_out, g_decode_trace, sizeof(g_decode_trace)));
+  return MEDHA_OK;
+}
+#endif
 
 medha_status medha_hbm_read_probe(const void *src, size_t bytes, float *sink, void *stream) {
   if (!src || !sink) return fail(MEDHA_EINVAL, "null argument");

@@ -41,9 +41,22 @@ def main():
         if not all(torch.equal(g[0], x) for x in g):
             fails.append(f"{what}: ranks differ")
 
-    # ---- decode: Eq. 5 -----------------------------------------------------------------
+    # ---- decode: Eq. 5 (fused NVLink exchange when available, and the NCCL path) -------
     q = synth.queries(11, 2, h_kv * G, d, amp=8.0)
     qp = [N - 1, N // 3]
+    p2p = comm.p2p
+    if world > 1 and not p2p:
+        fails.append("fused P2P exchange did not initialise")
+    if p2p:
+        comm.set_p2p(False)
+        o_n, lse_n, _ = M.kvp_decode(comm, [sh, sh], q.cuda(), qp)
+        o_n, lse_n = o_n.clone(), lse_n.clone()
+        comm.set_p2p(True)
+        for _ in range(3):          # several epochs through the double-buffered slots
+            o, lse, ob = M.kvp_decode(comm, [sh, sh], q.cuda(), qp, want_bf16=True)
+        torch.cuda.synchronize()
+        if (o - o_n).abs().max().item() > 1e-6 or (lse - lse_n).abs().max().item() > 1e-6:
+            fails.append(f"p2p vs nccl exchange differ: {(o - o_n).abs().max().item()}")
     o, lse, ob = M.kvp_decode(comm, [sh, sh], q.cuda(), qp, want_bf16=True)
     torch.cuda.synchronize()
     allsame(o, "kvp_decode o")
