@@ -20,9 +20,13 @@
 //     PRMT.  Query heads sit on the MMA M dimension (rows g and g+8).
 //   * fp32 online softmax in base 2 (scale*log2e folded into one multiply);
 //     P rounded to bf16 (RNE) before the PV MMA (reading R8).
-// Per-CTA: 4 warps interleave 16-token tiles; their (m, l, O) are merged through
-// shared memory; the CTA writes a normalised (o, lse2) split partial; the last
-// CTA of a (seq, kv head) (atomic ticket) merges all splits in split order.
+// Work items: one (seq, kv head, split) = a FIXED token range.  The grid is persistent
+// (2 CTAs per SM) and CTAs take items from an atomic queue, so faster SMs take more items
+// (HBM bandwidth per SM varies by ~10%) while every item's arithmetic - and therefore the
+// result - stays independent of which CTA ran it (bit-reproducible).  Per item: 4 warps
+// interleave 16-token tiles; their (m, l, O) are merged through shared memory; the item
+// writes a normalised (o, lse2) split partial; the CTA finishing the last split of a
+// (seq, kv head) (atomic ticket) merges all splits in split order (warp-parallel).
 #pragma once
 #include "common.cuh"
 
@@ -31,13 +35,13 @@ namespace medha {
 #ifdef MEDHA_DECODE_TRACE
 // experiment-only instrumentation: %globaltimer per CTA at start / main-loop end / partial
 // written / split merge done (read back with medha_debug_decode_trace)
-__device__ unsigned long long g_decode_trace[8192][8];
+__device__ unsigned long long g_decode_trace[8192][8];   // indexed by work item
 #define MEDHA_TRACE(k)                                                                     \
   do {                                                                                     \
-    if (threadIdx.x == 0 && blockIdx.x < 8192) {                                           \
+    if (threadIdx.x == 0 && item < 8192) {                                                 \
       unsigned long long t_;                                                               \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
-      g_decode_trace[blockIdx.x][k] = t_;                                                  \
+      g_decode_trace[item][k] = t_;                                                        \
     }                                                                                      \
   } while (0)
 #else
@@ -46,7 +50,8 @@ __device__ unsigned long long g_decode_trace[8192][8];
 
 constexpr int kDecodeMaxSeqPerLaunch = 64;
 constexpr int kMaxKvpRanks = 8;
-constexpr int kDecodeMaxSplits = 256;  // per (seq, kv head): the merge weights live in sm_o
+constexpr int kDecodeMaxSplits = 256;  // per (seq, kv head)
+constexpr int kDecodeSplitW = 2048;    // smem floats for split weights: splits <= kDecodeSplitW / G
 constexpr int kDecodeWarps = 4;
 constexpr int kDecodeThreads = kDecodeWarps * 32;
 
@@ -67,8 +72,10 @@ struct DecodeParams {
   float *lse;              // [batch][h_q], natural log
   float *ws_o;             // [slot][G][D] normalised split outputs
   float *ws_lse;           // [slot][G] base-2 split lse
-  unsigned *counters;      // [n_seq * h_kv]
+  unsigned *counters;      // [n_seq * h_kv] split tickets, then [2] work queue / exit counters
+  unsigned *work;          // persistent scheduler: work[0] next item, work[1] CTAs finished
   float scale_log2;        // softmax scale * log2(e)
+  int32_t n_items;         // (seq, kv head, split) work items of this launch
   int32_t n_seq;
   int32_t h_kv;
   int32_t h_q;
@@ -103,19 +110,23 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *ptr) {
 }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const __grid_constant__ DecodeParams p) {
-  static_assert(D == 64 || D == 128, "D");
-  static_assert(G >= 1 && G <= 16, "G");
+struct __align__(16) DecodeSmem {
+  float o[kDecodeWarps][G][D];   // warp partials; later the warp sums of the split merge
+  float m[kDecodeWarps][G];
+  float l[kDecodeWarps][G];
+  float w[kDecodeSplitW];        // split (or rank) merge weights [split][G]
+  unsigned ticket;
+  int item;
+};
+
+// One work item: split `split` of kv head `kvh` of sequence `sidx`.
+template <int D, int G>
+__device__ __forceinline__ void decode_item(const DecodeParams &p, const int item, DecodeSmem<D, G> &sm) {
   constexpr int KCH = D / 32;   // 16-byte K chunks per lane per token
   constexpr int VCH = D / 64;   // 16-byte V chunks per lane per token
   constexpr int KS = D / 16;    // k-steps of the QK MMA
   constexpr int NT = D / 8;     // n-tiles of the PV MMA
   constexpr bool kHi = (G > 8); // rows g+8 carry heads 8..15
-
-  __shared__ float sm_o[kDecodeWarps][G][D];
-  __shared__ float sm_m[kDecodeWarps][G];
-  __shared__ float sm_l[kDecodeWarps][G];
-  __shared__ unsigned sm_ticket;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -123,11 +134,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
   const int g = lane >> 2;
   const int c = lane & 3;
 
-  // ---- which (sequence, kv head, split) is this CTA -------------------------------
   int sidx = 0;
-  while (sidx + 1 < p.n_seq && (int)blockIdx.x >= p.seq[sidx + 1].cta_begin) ++sidx;
+  while (sidx + 1 < p.n_seq && item >= p.seq[sidx + 1].cta_begin) ++sidx;
   const DecodeSeq &S = p.seq[sidx];
-  const int local = (int)blockIdx.x - S.cta_begin;
+  const int local = item - S.cta_begin;
   const int kvh = local / S.n_splits;
   const int split = local - kvh * S.n_splits;
   const int64_t t_begin = (int64_t)split * S.split_tokens;
@@ -286,8 +296,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
   }
   if (c == 0) {
-    if (g < G) { sm_m[warp][g] = m_lo; sm_l[warp][g] = l_lo; }
-    if (kHi && g + 8 < G) { sm_m[warp][g + 8] = m_hi; sm_l[warp][g + 8] = l_hi; }
+    if (g < G) { sm.m[warp][g] = m_lo; sm.l[warp][g] = l_lo; }
+    if (kHi && g + 8 < G) { sm.m[warp][g + 8] = m_hi; sm.l[warp][g + 8] = l_hi; }
   }
   // O fragment n-tile j, element e in {0,1}: head row g (+8), d = 64*(j/8) + 8*(2c+e) + (j%8)
 #pragma unroll
@@ -295,28 +305,28 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int dd = 64 * (j >> 3) + 8 * (2 * c + e) + (j & 7);
-      if (g < G) sm_o[warp][g][dd] = oacc[j][e];
-      if (kHi && g + 8 < G) sm_o[warp][g + 8][dd] = oacc[j][2 + e];
+      if (g < G) sm.o[warp][g][dd] = oacc[j][e];
+      if (kHi && g + 8 < G) sm.o[warp][g + 8][dd] = oacc[j][2 + e];
     }
   }
   __syncthreads();
 
   // ---- CTA merge of the 4 warps: (o normalised, lse2) of this split ---------------------
-  const bool single = (S.n_splits == 1);
+  const bool single = (S.n_splits == 1);   // (never with the fused exchange: host plans >= 2)
   const int64_t slot = (int64_t)S.slot_begin + (int64_t)kvh * S.n_splits + split;
   float *dst_o = single ? (p.o + ((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D) : (p.ws_o + slot * G * D);
   for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
     const int row = idx / D, dd = idx - row * D;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kDecodeWarps; ++w) M = fmaxf(M, sm_m[w][row]);
+    for (int w = 0; w < kDecodeWarps; ++w) M = fmaxf(M, sm.m[w][row]);
     float L = 0.f, acc = 0.f;
     if (M != -INFINITY) {
 #pragma unroll
       for (int w = 0; w < kDecodeWarps; ++w) {
-        const float sc = exp2_int(sm_m[w][row] - M);
-        L += sm_l[w][row] * sc;
-        acc += sm_o[w][row][dd] * sc;
+        const float sc = exp2_int(sm.m[w][row] - M);
+        L += sm.l[w][row] * sc;
+        acc += sm.o[w][row][dd] * sc;
       }
     }
     dst_o[idx] = (L > 0.f) ? acc / L : 0.f;
@@ -331,35 +341,34 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
   MEDHA_TRACE(2);
   if (single) return;
 
-  // ---- last CTA of this (seq, kv head) merges the splits in split order -----------------
+  // ---- the CTA finishing the last split of this (seq, kv head) merges the splits --------
   __threadfence();
   __syncthreads();
   unsigned *ctr = p.counters + (int64_t)sidx * p.h_kv + kvh;
-  if (tid == 0) sm_ticket = atomicAdd(ctr, 1u);
+  if (tid == 0) sm.ticket = atomicAdd(ctr, 1u);
   __syncthreads();
-  if (sm_ticket != (unsigned)(S.n_splits - 1)) return;
+  if (sm.ticket != (unsigned)(S.n_splits - 1)) return;
   __threadfence();
   const int64_t slot0 = (int64_t)S.slot_begin + (int64_t)kvh * S.n_splits;
-  const int ns = S.n_splits;                 // <= kDecodeMaxSplits (host planner)
-  float *smw = &sm_o[0][0][0];               // [ns][G] merge weights; warp partials are dead
-  for (int i = tid; i < ns * G; i += kDecodeThreads) smw[i] = __ldcg(p.ws_lse + slot0 * G + i);
+  const int ns = S.n_splits;                 // <= kDecodeSplitW / G (host planner)
+  for (int i = tid; i < ns * G; i += kDecodeThreads) sm.w[i] = __ldcg(p.ws_lse + slot0 * G + i);
   __syncthreads();
   // per row: M = max_s lse_s, w_s = 2^(lse_s - M) / sum_s 2^(lse_s - M)   (one warp per row)
   for (int row = warp; row < G; row += kDecodeWarps) {
     float M = -INFINITY;
-    for (int s2 = lane; s2 < ns; s2 += 32) M = fmaxf(M, smw[s2 * G + row]);
+    for (int s2 = lane; s2 < ns; s2 += 32) M = fmaxf(M, sm.w[s2 * G + row]);
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
     float L = 0.f;
     for (int s2 = lane; s2 < ns; s2 += 32) {
-      const float w = (M == -INFINITY) ? 0.f : fast_exp2(smw[s2 * G + row] - M);
-      smw[s2 * G + row] = w;
+      const float w = (M == -INFINITY) ? 0.f : fast_exp2(sm.w[s2 * G + row] - M);
+      sm.w[s2 * G + row] = w;
       L += w;
     }
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
     const float inv = (L > 0.f) ? 1.f / L : 0.f;
-    for (int s2 = lane; s2 < ns; s2 += 32) smw[s2 * G + row] *= inv;
+    for (int s2 = lane; s2 < ns; s2 += 32) sm.w[s2 * G + row] *= inv;
     if (lane == 0) {
       const float lse_r = (L > 0.f) ? (M + __log2f(L)) * kLn2 : -INFINITY;
       const int64_t orow = (int64_t)sidx * p.h_q + (int64_t)kvh * G + row;
@@ -371,62 +380,83 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     }
   }
   __syncthreads();
-  // outputs: every thread owns OPT outputs and streams the splits in batches of SB, so
-  // OPT*SB independent L2 loads are in flight (the merge sits on the kernel's critical
-  // path: one latency round per batch); summed in split order (deterministic).
-  constexpr int OPT = (G * D + kDecodeThreads - 1) / kDecodeThreads;   // 1..16 outputs per thread
-  const bool own0 = tid < G * D;                                        // (G*D = 64 for G=1, D=64)
-  constexpr int SB = OPT >= 8 ? 4 : 8;
-  const float *src0 = p.ws_o + slot0 * G * D + tid;
-  float acc[OPT];
+  // warp-parallel: warp w sums splits w, w+4, ...; lane owns float4 chunks of the G*D
+  // outputs; SB splits per batch keep 4*NV*SB loads in flight (one L2 latency per batch)
+  {
+    constexpr int NV = (G * D / 4 + 31) / 32;   // float4 chunks per lane (1..16)
+    constexpr int SB = NV >= 8 ? 2 : (NV >= 4 ? 4 : 8);
+    const float4 *src0 = reinterpret_cast<const float4 *>(p.ws_o + slot0 * G * D);
+    float4 acc[NV];
 #pragma unroll
-  for (int i = 0; i < OPT; ++i) acc[i] = 0.f;
-  for (int s2 = 0; s2 < ns; s2 += SB) {
-    float v[SB][OPT];
+    for (int i = 0; i < NV; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s2 = warp; s2 < ns; s2 += kDecodeWarps * SB) {
+      float4 v[SB][NV];
 #pragma unroll
-    for (int u = 0; u < SB; ++u)
+      for (int u = 0; u < SB; ++u)
 #pragma unroll
-      for (int i = 0; i < OPT; ++i)
-        v[u][i] = (s2 + u < ns && own0) ? __ldcg(src0 + (int64_t)(s2 + u) * G * D + i * kDecodeThreads) : 0.f;
+        for (int i = 0; i < NV; ++i) {
+          const int ch = lane + 32 * i;
+          const int ss = s2 + u * kDecodeWarps;
+          v[u][i] = (ss < ns && ch < G * D / 4) ? __ldcg(src0 + (int64_t)ss * (G * D / 4) + ch)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-    for (int u = 0; u < SB; ++u)
+      for (int u = 0; u < SB; ++u)
 #pragma unroll
-      for (int i = 0; i < OPT; ++i)
-        if (s2 + u < ns && own0) acc[i] = fmaf(smw[(s2 + u) * G + (tid + i * kDecodeThreads) / D], v[u][i], acc[i]);
+        for (int i = 0; i < NV; ++i) {
+          const int ch = lane + 32 * i;
+          const int ss = s2 + u * kDecodeWarps;
+          if (ss < ns && ch < G * D / 4) {
+            const float w = sm.w[ss * G + (4 * ch) / D];
+            acc[i].x = fmaf(w, v[u][i].x, acc[i].x);
+            acc[i].y = fmaf(w, v[u][i].y, acc[i].y);
+            acc[i].z = fmaf(w, v[u][i].z, acc[i].z);
+            acc[i].w = fmaf(w, v[u][i].w, acc[i].w);
+          }
+        }
+    }
+    float4 *wsum = reinterpret_cast<float4 *>(&sm.o[warp][0][0]);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (lane + 32 * i < G * D / 4) wsum[lane + 32 * i] = acc[i];
   }
-  const int64_t obase = ((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D + tid;
+  __syncthreads();
+  const int64_t obase = ((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D;
+  for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
+    const float *w0 = &sm.o[0][0][0];
+    constexpr int WS = G * D;   // one warp's [G][D] block
+    const float o = ((w0[idx] + w0[WS + idx]) + w0[2 * WS + idx]) + w0[3 * WS + idx];   // fixed order
+    if (p.x_world > 0) {
+      for (int r = 0; r < p.x_world; ++r) p.x_dst[r][obase + idx] = o;                   // NVLink stores
+    } else {
+      p.o[obase + idx] = o;
+    }
+  }
   if (tid == 0) *ctr = 0u;  // leave the counter zeroed for the next call
-  if (p.x_world == 0) {
-#pragma unroll
-    for (int i = 0; i < OPT; ++i)
-      if (own0) p.o[obase + i * kDecodeThreads] = acc[i];
-    MEDHA_TRACE(3);
-    return;
+  if (p.x_world > 0) {
+    __syncthreads();
+    // one system-scope fence after the barrier orders every thread's NVLink stores before
+    // the flag stores (cumulativity through bar.sync)
+    if (tid == 0) __threadfence_system();
+    __syncthreads();
+    const int unit = sidx * p.h_kv + kvh;
+    if (tid < p.x_world) st_release_sys(p.x_flag_dst[tid] + unit, p.x_epoch);
   }
-  // ---- fused KVP exchange: push this unit's partial to every rank, then merge ----------
-  for (int r = 0; r < p.x_world; ++r) {
-#pragma unroll
-    for (int i = 0; i < OPT; ++i)
-      if (own0) p.x_dst[r][obase + i * kDecodeThreads] = acc[i];                 // NVLink stores
-  }
-  MEDHA_TRACE(4);
-  __syncthreads();
-  // one system-scope fence after the barrier orders every thread's NVLink stores before
-  // the flag stores (cumulativity through bar.sync)
-  if (tid == 0) __threadfence_system();
-  __syncthreads();
-  MEDHA_TRACE(5);
-  const int unit = sidx * p.h_kv + kvh;
+  MEDHA_TRACE(3);
+}
+
+// Fused exchange, second half: wait until every rank's partial of `unit` has arrived
+// (acquire) and merge them in rank order (same formula as lse_merge_kernel).
+template <int D, int G>
+__device__ __forceinline__ void xchg_merge_unit(const DecodeParams &p, const int unit, DecodeSmem<D, G> &sm) {
+  const int tid = threadIdx.x;
+  const int sidx = unit / p.h_kv, kvh = unit - sidx * p.h_kv;
   if (tid < p.x_world) {
-    st_release_sys(p.x_flag_dst[tid] + unit, p.x_epoch);
     const uint32_t *f = p.x_flags + (int64_t)tid * p.x_units + unit;
     while (ld_acquire_sys(f) != p.x_epoch) {
     }
   }
   __syncthreads();
-  MEDHA_TRACE(6);
-  // merge in rank order (same formula and order as lse_merge_kernel): identical on all ranks
-  float *xw = smw;                                  // [x_world][G] weights
   const int64_t lrow0 = p.x_rows * D + (int64_t)sidx * p.h_q + (int64_t)kvh * G;
   if (tid < G) {
     const int row = tid;
@@ -439,26 +469,54 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
       lse_f = M + __logf(ssum);
     }
     for (int r = 0; r < p.x_world; ++r)
-      xw[r * G + row] = (M == -INFINITY) ? 0.f : __expf(__ldcg(p.x_recv + (int64_t)r * p.x_slot + lrow0 + row) - lse_f);
+      sm.w[r * G + row] = (M == -INFINITY) ? 0.f : __expf(__ldcg(p.x_recv + (int64_t)r * p.x_slot + lrow0 + row) - lse_f);
     if (p.x_lse) p.x_lse[(int64_t)sidx * p.h_q + (int64_t)kvh * G + row] = lse_f;
   }
   __syncthreads();
-#pragma unroll
-  for (int i = 0; i < OPT; ++i) {
-    if (!own0) break;
-    const int row = (tid + i * kDecodeThreads) / D;
+  const int64_t obase = ((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D;
+  for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
+    const int row = idx / D;
     float v[kMaxKvpRanks];
 #pragma unroll
-    for (int r = 0; r < kMaxKvpRanks; ++r)
-      v[r] = (r < p.x_world) ? __ldcg(p.x_recv + (int64_t)r * p.x_slot + obase + i * kDecodeThreads) : 0.f;
+    for (int r = 0; r < kMaxKvpRanks; ++r) v[r] = (r < p.x_world) ? __ldcg(p.x_recv + (int64_t)r * p.x_slot + obase + idx) : 0.f;
     float o = 0.f;
 #pragma unroll
     for (int r = 0; r < kMaxKvpRanks; ++r)
-      if (r < p.x_world) o += xw[r * G + row] * v[r];
-    p.x_o[obase + i * kDecodeThreads] = o;
-    if (p.x_obf) p.x_obf[obase + i * kDecodeThreads] = __float2bfloat16_rn(o);
+      if (r < p.x_world) o += sm.w[r * G + row] * v[r];
+    p.x_o[obase + idx] = o;
+    if (p.x_obf) p.x_obf[obase + idx] = __float2bfloat16_rn(o);
   }
-  MEDHA_TRACE(3);
+  __syncthreads();
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const __grid_constant__ DecodeParams p) {
+  static_assert(D == 64 || D == 128, "D");
+  static_assert(G >= 1 && G <= 16, "G");
+  static_assert(kDecodeMaxSplits * G <= kDecodeSplitW || G > 8, "split weights");
+  __shared__ DecodeSmem<D, G> sm;
+  // persistent: take work items from the queue until it runs dry
+  for (;;) {
+    if (threadIdx.x == 0) sm.item = (int)atomicAdd(p.work, 1u);
+    __syncthreads();
+    const int item = sm.item;
+    __syncthreads();
+    if (item >= p.n_items) break;
+    decode_item<D, G>(p, item, sm);
+    __syncthreads();
+  }
+  // fused KVP exchange: units are merged after this CTA's items (no CTA ever spins while
+  // this rank still has unprocessed items, so the wait cannot deadlock)
+  if (p.x_world > 0)
+    for (int unit = blockIdx.x; unit < p.n_seq * p.h_kv; unit += gridDim.x) xchg_merge_unit<D, G>(p, unit, sm);
+  // the last CTA out resets the queue for the next launch
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.work + 1, 1u) == gridDim.x - 1) {
+      p.work[0] = 0u;
+      p.work[1] = 0u;
+    }
+  }
 }
 
 }  // namespace medha

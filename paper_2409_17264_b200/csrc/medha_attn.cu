@@ -86,7 +86,16 @@ medha_status check_shard(const medha_kv_shard *kv) {
 // ---------------------------------------------------------------------------------------------
 // decode
 // ---------------------------------------------------------------------------------------------
-constexpr int kDecodeCtaBudget = 1024;  // upper bound of split CTAs per launch (workspace sizing)
+constexpr int kDecodeMaxKvHeads = 64;
+constexpr int kDecodeWorkWord = kDecodeMaxSeqPerLaunch * kDecodeMaxKvHeads;   // tickets [seq][kv head] before it
+constexpr int kDecodeCounterWords = kDecodeWorkWord + 64;
+constexpr int kDecodeCtaBudget = 4096;  // upper bound of work items (splits) per launch (workspace sizing)
+#ifndef MEDHA_DEC_ITEMS
+#define MEDHA_DEC_ITEMS 1        // work items per resident CTA slot (A/B on B200: 1 > 2 > 4)
+#endif
+#ifndef MEDHA_DEC_MIN_SPLIT
+#define MEDHA_DEC_MIN_SPLIT 256  // minimum tokens per split (short contexts: more CTAs, shorter chains)
+#endif
 
 struct DecodeWs {
   unsigned *counters;
@@ -100,8 +109,10 @@ size_t decode_ws_layout(int32_t batch, int32_t h_q, int32_t h_kv, int32_t d, cha
   const int64_t G = h_kv > 0 ? h_q / h_kv : 1;
   const int64_t slots = kDecodeCtaBudget + nb * h_kv;
   size_t off = 0;
+  // counters live at a FIXED place and size whatever the call shape, so the "left zeroed"
+  // invariant of the header holds across calls with different batch / h_kv / d
   const size_t c_off = off;
-  off = round_up(off + nb * h_kv * sizeof(unsigned), 256);
+  off = round_up(off + kDecodeCounterWords * sizeof(unsigned), 256);   // split tickets + work queue
   const size_t l_off = off;
   off = round_up(off + slots * G * sizeof(float), 256);
   const size_t o_off = off;
@@ -157,6 +168,7 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
   if (!aligned16(q)) return fail(MEDHA_EINVAL, "q not 16-byte aligned");
   if (!(scale > 0.f)) return fail(MEDHA_EINVAL, "scale must be > 0");
   const int32_t h_kv = kvs[0].h_kv, d = kvs[0].d;
+  if (h_kv > kDecodeMaxKvHeads) return fail(MEDHA_ENOTSUP, "h_kv %d > %d", h_kv, kDecodeMaxKvHeads);
   for (int b = 0; b < batch; ++b) {
     medha_status s = check_shard(&kvs[b]);
     if (s) return s;
@@ -171,7 +183,9 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
   if (ws_bytes < W.bytes) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, W.bytes);
 
   if (x && batch > kDecodeMaxSeqPerLaunch) return fail(MEDHA_ENOTSUP, "fused exchange needs batch <= 64");
-  const int target = 2 * num_sms();  // two 4-warp CTAs per SM
+  const int slots = 2 * num_sms();                 // two 4-warp CTAs per SM, persistent
+  const int target = MEDHA_DEC_ITEMS * slots;       // work items per launch
+  const int max_splits = std::min(kDecodeMaxSplits, kDecodeSplitW / G);
   for (int b0 = 0; b0 < batch; b0 += kDecodeMaxSeqPerLaunch) {
     const int nb = std::min(kDecodeMaxSeqPerLaunch, batch - b0);
     DecodeParams p;
@@ -182,6 +196,7 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
     p.ws_o = W.ws_o;
     p.ws_lse = W.ws_lse;
     p.counters = W.counters;
+    p.work = W.counters + kDecodeWorkWord;
     p.scale_log2 = scale * kLog2e;
     p.n_seq = nb;
     p.h_kv = h_kv;
@@ -210,11 +225,12 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
       nvis[i] = std::max<int64_t>(0, std::min<int64_t>(kv.len, q_pos[b0 + i] - kv.pos0 + 1));
       total += nvis[i] * h_kv;
     }
-    const int64_t per_cta = std::max<int64_t>(256, round_up((size_t)cdiv(std::max<int64_t>(total, 1), target), 64));
+    const int64_t per_cta =
+        std::max<int64_t>(MEDHA_DEC_MIN_SPLIT, round_up((size_t)cdiv(std::max<int64_t>(total, 1), target), 64));
     int cta = 0;
     for (int i = 0; i < nb; ++i) {
       const medha_kv_shard &kv = kvs[b0 + i];
-      int64_t ns = std::min<int64_t>(kDecodeMaxSplits, std::max<int64_t>(1, cdiv(nvis[i], per_cta)));
+      int64_t ns = std::min<int64_t>(max_splits, std::max<int64_t>(1, cdiv(nvis[i], per_cta)));
       int64_t split_tokens = std::max<int64_t>(64, (int64_t)round_up((size_t)cdiv(std::max<int64_t>(nvis[i], 1), ns), 64));
       ns = std::max<int64_t>(1, cdiv(nvis[i], split_tokens));
       if (x && ns < 2) ns = 2;  // the exchange runs in the split-merging last CTA
@@ -231,7 +247,9 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
       cta += (int)(ns * h_kv);
     }
     if (cta > kDecodeCtaBudget + nb * h_kv) return fail(MEDHA_EWORKSPACE, "split plan exceeds workspace");
-    medha_status s = (d == 128) ? dispatch_decode_g<128>(G, p, cta, st) : dispatch_decode_g<64>(G, p, cta, st);
+    p.n_items = cta;
+    const int grid = std::min(cta, slots);
+    medha_status s = (d == 128) ? dispatch_decode_g<128>(G, p, grid, st) : dispatch_decode_g<64>(G, p, grid, st);
     if (s) return s;
   }
   return MEDHA_OK;

@@ -12,9 +12,9 @@ for n in (1 << 20, 1 << 18, 1 << 17):
     for _ in range(5): M.attn_decode_partial([sh], q, [n - 1], o=o, lse=l, ws=ws)
     a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
     a.record(); M.attn_decode_partial([sh], q, [n - 1], o=o, lse=l, ws=ws); b.record(); torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (8192 * 4))()
+    buf = (ctypes.c_ulonglong * (8192 * 8))()
     M.lib.medha_debug_decode_trace(buf)
-    t = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 4).astype(np.int64)
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 8).astype(np.int64)
     used = t[:296]
     t0 = used[:, 0].min()
     st, loop, part = (used[:, 0] - t0) / 1e3, (used[:, 1] - t0) / 1e3, (used[:, 2] - t0) / 1e3
