@@ -36,6 +36,14 @@ __device__ __forceinline__ float bf16x2_sum(uint32_t u) {
   return __uint_as_float(u << 16) + __uint_as_float(u & 0xffff0000u);
 }
 
+// acc_lo += bf16 low half of u, acc_hi += bf16 high half (sm_100 mixed-precision add:
+// one FHADD.BF16 per element reading the half register, no unpack instructions)
+__device__ __forceinline__ void add_bf16x2_f32(float &acc_lo, float &acc_hi, uint32_t u) {
+  asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %2;\n add.rn.f32.bf16 %0, lo, %0;\n add.rn.f32.bf16 %1, hi, %1;\n}"
+      : "+f"(acc_lo), "+f"(acc_hi)
+      : "r"(u));
+}
+
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));

@@ -261,8 +261,18 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
     const uint32_t a2 = pack_bf16x2(pr[1][0], pr[1][1]);
     const uint32_t a3 = kHi ? pack_bf16x2(pr[1][2], pr[1][3]) : 0u;
     // the normaliser sums the bf16-rounded P the MMA consumes (consistent weights)
-    l_lo = l_lo * al_lo + (bf16x2_sum(a0) + bf16x2_sum(a2));
-    if (kHi) l_hi = l_hi * al_hi + (bf16x2_sum(a1) + bf16x2_sum(a3));
+    {
+      float t0 = 0.f, t1 = 0.f;
+      add_bf16x2_f32(t0, t1, a0);
+      add_bf16x2_f32(t0, t1, a2);
+      l_lo = l_lo * al_lo + (t0 + t1);
+      if (kHi) {
+        float u0 = 0.f, u1 = 0.f;
+        add_bf16x2_f32(u0, u1, a1);
+        add_bf16x2_f32(u0, u1, a3);
+        l_hi = l_hi * al_hi + (u0 + u1);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const int ch = j >> 3, e = j & 7;

@@ -39,6 +39,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef MEDHA_PF_SETMAXNREG
 #define MEDHA_PF_SETMAXNREG 0   // rebalance registers between warpgroups (A/B knob)
 #endif
+#ifndef MEDHA_PF_RAW_L
+#define MEDHA_PF_RAW_L 0   // normaliser: 0 rounded P via FHADD.BF16 (R20), 1 unrounded P, 2 rounded P via unpack
+#endif
 #ifndef MEDHA_PF_POLY_NUM      // fraction NUM/DEN of column pairs whose exp2 runs on the FMA pipe
 #define MEDHA_PF_POLY_NUM 0
 #endif
@@ -155,7 +158,13 @@ __device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[12
         pp.y = (col + 1 < nvalid) ? pp.y : 0.f;
       }
       pk[e >> 1] = pack_bf16x2(pp.x, pp.y);
+#if MEDHA_PF_RAW_L == 1
+      lsum2 = __fadd2_rn(lsum2, pp);   // A/B: normaliser of the unrounded P
+#elif MEDHA_PF_RAW_L == 2
       lsum2 = __fadd2_rn(lsum2, make_float2(__uint_as_float(pk[e >> 1] << 16), __uint_as_float(pk[e >> 1] & 0xffff0000u)));
+#else
+      add_bf16x2_f32(lsum2.x, lsum2.y, pk[e >> 1]);   // rounded P, one FHADD.BF16 per element
+#endif
     }
     tmem_st16(tS + 16 * q, pk);
   }
