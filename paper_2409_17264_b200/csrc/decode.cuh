@@ -48,6 +48,10 @@ __device__ unsigned long long g_decode_trace[8192][8];   // indexed by work item
 #define MEDHA_TRACE(k) do {} while (0)
 #endif
 
+#ifndef MEDHA_DEC_PINGPONG
+#define MEDHA_DEC_PINGPONG 1   // 2x-unrolled main loop with ping-pong K/V register buffers
+#endif
+
 constexpr int kDecodeMaxSeqPerLaunch = 64;
 constexpr int kMaxKvpRanks = 8;
 constexpr int kDecodeMaxSplits = 256;  // per (seq, kv head)
@@ -166,7 +170,6 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   float m_lo = -INFINITY, m_hi = -INFINITY;  // running max (base 2) of rows g, g+8
   float l_lo = 0.f, l_hi = 0.f;              // thread-partial running sums
 
-  uint4 kr[2][KCH], vr[4][VCH];
   auto load_tile = [&](int64_t tb, uint4 (&kk)[2][KCH], uint4 (&vv)[4][VCH]) {
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
@@ -186,14 +189,8 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
     }
   };
 
-  MEDHA_TRACE(0);
-  int64_t tb = t_begin + 16 * warp;
-  if (tb < t_end) load_tile(tb, kr, vr);
-  for (; tb < t_end; tb += 16 * kDecodeWarps) {
-    uint4 kn[2][KCH], vn[4][VCH];
-    const int64_t nb = tb + 16 * kDecodeWarps;
-    if (nb < t_end) load_tile(nb, kn, vn);
-
+  // one 16-token tile: S = QK^T, online softmax, O += PV (K/V fragments in registers)
+  auto compute_tile = [&](const uint4 (&kr)[2][KCH], const uint4 (&vr)[4][VCH], const int64_t tb) {
     // ---- S = Q K^T  (rows: heads g / g+8; cols: tokens 2c,2c+1 of n-tile n) ----------
     float s[2][4];
 #pragma unroll
@@ -285,6 +282,33 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
       const uint32_t b1 = prmt(r2[e >> 1], r3[e >> 1], sel);
       mma_bf16_16816(oacc[j], a0, a1, a2, a3, b0, b1);
     }
+  };
+
+  MEDHA_TRACE(0);
+  constexpr int64_t kStep = 16 * kDecodeWarps;
+  int64_t tb = t_begin + 16 * warp;
+#if MEDHA_DEC_PINGPONG
+  // 2x unrolled with ping-pong register buffers: tile i+1 loads while tile i computes,
+  // without copying the prefetched fragments between iterations
+  uint4 kb0[2][KCH], vb0[4][VCH], kb1[2][KCH], vb1[4][VCH];
+  if (tb < t_end) load_tile(tb, kb0, vb0);
+  while (tb < t_end) {
+    if (tb + kStep < t_end) load_tile(tb + kStep, kb1, vb1);
+    compute_tile(kb0, vb0, tb);
+    tb += kStep;
+    if (tb >= t_end) break;
+    if (tb + kStep < t_end) load_tile(tb + kStep, kb0, vb0);
+    compute_tile(kb1, vb1, tb);
+    tb += kStep;
+  }
+#else
+  uint4 kr[2][KCH], vr[4][VCH];
+  if (tb < t_end) load_tile(tb, kr, vr);
+  for (; tb < t_end; tb += kStep) {
+    uint4 kn[2][KCH], vn[4][VCH];
+    const int64_t nb = tb + kStep;
+    if (nb < t_end) load_tile(nb, kn, vn);
+    compute_tile(kr, vr, tb);
     if (nb < t_end) {
 #pragma unroll
       for (int n = 0; n < 2; ++n)
@@ -296,6 +320,7 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
         for (int i = 0; i < VCH; ++i) vr[r][i] = vn[r][i];
     }
   }
+#endif
 
   MEDHA_TRACE(1);
   // ---- per-warp reduction of l over the 4 lanes of a row, publish to smem --------------

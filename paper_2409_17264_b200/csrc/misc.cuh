@@ -30,25 +30,44 @@ __global__ void lse_merge_kernel(const float *__restrict__ parts, int32_t P, int
                                  float *__restrict__ o_out, float *__restrict__ lse_out,
                                  __nv_bfloat16 *__restrict__ o_bf16) {
   constexpr int PER = D / 32;  // floats per lane: d = lane + 32 i (coalesced; parts are packed, no alignment beyond 4 B)
+  constexpr int U = 8;         // parts whose o rows are loaded together (latency hiding)
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
-  const float *lse_base = parts + rows * D + row;
-  float M = -INFINITY;
-  for (int r = 0; r < P; ++r) M = fmaxf(M, lse_base[(int64_t)r * part_stride]);
+  // lane r (and r + 32) holds part r's lse (P <= 64)
+  const float *lse_col = parts + rows * D + row;
+  const float l0 = (lane < P) ? lse_col[(int64_t)lane * part_stride] : -INFINITY;
+  const float l1 = (lane + 32 < P) ? lse_col[(int64_t)(lane + 32) * part_stride] : -INFINITY;
+  float M = fmaxf(l0, l1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   float acc[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) acc[i] = 0.f;
   float lse = -INFINITY;
   if (M != -INFINITY) {
-    float s = 0.f;
-    for (int r = 0; r < P; ++r) s += __expf(lse_base[(int64_t)r * part_stride] - M);
-    lse = M + __logf(s);
-    for (int r = 0; r < P; ++r) {
-      const float w = __expf(lse_base[(int64_t)r * part_stride] - lse);
-      const float *orow = parts + (int64_t)r * part_stride + row * D;
+    float s = __expf(l0 - M) + __expf(l1 - M);
 #pragma unroll
-      for (int i = 0; i < PER; ++i) acc[i] += w * orow[lane + 32 * i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    lse = M + __logf(s);
+    const float w0 = __expf(l0 - lse), w1 = __expf(l1 - lse);
+    for (int r0 = 0; r0 < P; r0 += U) {
+      float v[U][PER];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float *orow = parts + (int64_t)(r0 + u) * part_stride + row * D;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) v[u][i] = (r0 + u < P) ? orow[lane + 32 * i] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = r0 + u;   // rank order 0..P-1
+        const float w = __shfl_sync(0xffffffffu, (r < 32) ? w0 : w1, r & 31);
+        if (r < P) {
+#pragma unroll
+          for (int i = 0; i < PER; ++i) acc[i] += w * v[u][i];
+        }
+      }
     }
   }
   float *od = o_out + row * D;
