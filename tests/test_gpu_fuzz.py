@@ -1,0 +1,59 @@
+"""Seeded random-shape parity sweep: decode and prefill vs the fp64 oracle over ragged
+lengths, shard offsets (pos0), causal cuts inside and before the shard, every supported
+group size and head dimension, and batches of unequal sequences."""
+import numpy as np
+import pytest
+
+import synth
+from helpers import compare, make_global_kv, oracle_attention, to_shard
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def M():
+    import paper_2409_17264_b200 as M
+    return M
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_fuzz_decode(M, case):
+    rng = np.random.default_rng(1000 + case)
+    d = int(rng.choice([64, 128]))
+    G = int(rng.choice([1, 2, 4, 8, 16]))
+    h_kv = int(rng.choice([1, 2, 3]))
+    B = int(rng.integers(1, 5))
+    shards, qs, qps, refs = [], [], [], []
+    for b in range(B):
+        N = int(rng.integers(1, 6000))
+        a = int(rng.integers(0, N))                    # shard = global tokens [a, N)
+        qpos = int(rng.integers(max(0, a - 20), N))     # may precede the shard (empty)
+        k, v = make_global_kv(2000 + 10 * case + b, N, h_kv, d)
+        q = synth.queries(2000 + 10 * case + b, 1, h_kv * G, d, amp=float(rng.choice([1.0, 4.0, 8.0])))
+        shards.append(to_shard(k, v, a, N, extra_cap=int(rng.integers(0, 50))))
+        qs.append(q)
+        qps.append(qpos)
+        refs.append(oracle_attention(q, k, v, [qpos], (a, N)))
+    import torch
+    o, lse = M.attn_decode_partial(shards, torch.cat(qs).cuda(), qps)
+    for b in range(B):
+        compare(o[b:b + 1], lse[b:b + 1], refs[b][0], refs[b][1], what=f"fuzz decode {case}/{b}")
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_fuzz_prefill(M, case):
+    rng = np.random.default_rng(3000 + case)
+    d = int(rng.choice([64, 128]))
+    G = int(rng.choice([1, 2, 4, 8, 16]))
+    h_kv = int(rng.choice([1, 2]))
+    c = int(rng.integers(1, 400))
+    P0 = int(rng.integers(0, 3000))
+    N = P0 + c
+    a = int(rng.integers(0, min(N, P0 + 1)))          # shard [a, N): contains the chunk's own keys
+    k, v = make_global_kv(4000 + case, N, h_kv, d)
+    q = synth.queries(4000 + case, c, h_kv * G, d, amp=float(rng.choice([1.0, 4.0, 8.0])), t0=P0)
+    sh = to_shard(k, v, a, N, extra_cap=int(rng.integers(0, 200)))
+    o, lse = M.attn_prefill_chunk(sh, q.cuda(), P0)
+    rows = sorted(set([0, c - 1] + [int(x) for x in rng.integers(0, c, size=min(c, 6))]))
+    ro, rl = oracle_attention(q[rows], k, v, [P0 + r for r in rows], (a, N))
+    compare(o[rows], lse[rows], ro, rl, what=f"fuzz prefill {case}: c={c} P0={P0} a={a} G={G} d={d}")
