@@ -39,6 +39,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef MEDHA_PF_SETMAXNREG
 #define MEDHA_PF_SETMAXNREG 0   // rebalance registers between warpgroups (A/B knob)
 #endif
+#ifndef MEDHA_PF_SPLIT_FMA
+#define MEDHA_PF_SPLIT_FMA 1   // x = (s*scale) - m in two roundings (partition-invariant P)
+#endif
 #ifndef MEDHA_PF_RAW_L
 #define MEDHA_PF_RAW_L 0   // normaliser: 0 rounded P via FHADD.BF16 (R20), 1 unrounded P, 2 rounded P via unpack
 #endif
@@ -140,13 +143,24 @@ __device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[12
                                              int nvalid) {
   float2 lsum2 = make_float2(0.f, 0.f);
   const float2 sl2v = make_float2(sl2, sl2), nmu = make_float2(-mu, -mu);
+  const float2 nmu384 = make_float2(-(384.f + mu), -(384.f + mu));   // exact: mu is an integer
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t pk[16];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
       const int col = 32 * q + e;
+#if MEDHA_PF_SPLIT_FMA
+      // t = s*scale + 1.5*2^8 rounds s*scale onto the fixed grid 2^-15 (depends on s only);
+      // x = t - (1.5*2^8 + m) is then EXACT for any integer m (|x| < 2^8), so P's bf16
+      // rounding does not depend on the partition's max: KVP == single GPU bit for bit
+      // up to fp32 summation order (grid error <= 2^-16 in x, 1e-5 relative in P)
+      const float2 t = __ffma2_rn(make_float2(__uint_as_float(s[col]), __uint_as_float(s[col + 1])), sl2v,
+                                  make_float2(384.f, 384.f));
+      const float2 x = __fadd2_rn(t, nmu384);
+#else
       const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[col]), __uint_as_float(s[col + 1])), sl2v, nmu);
+#endif
       float2 pp;
       if (!kMasked && ((col >> 1) % MEDHA_PF_POLY_DEN) < MEDHA_PF_POLY_NUM) {
         pp = ex2_poly2(x);

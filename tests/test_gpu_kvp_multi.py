@@ -19,11 +19,12 @@ def _port():
     return p
 
 
+@pytest.mark.parametrize("worker", ["kvp_worker.py", "kvp_worker_ext.py"])
 @pytest.mark.parametrize("P", [2, 4])
-def test_kvp_multi_gpu(P):
+def test_kvp_multi_gpu(P, worker):
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tests", "kvp_worker.py")]
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tests", worker)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]

@@ -84,3 +84,17 @@ def test_shard_range_partitions_exactly():
             assert all(rs[i][1] == rs[i + 1][0] for i in range(P - 1))
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+def test_growth_placement():
+    from paper_2409_17264_b200.kvp import growth_placement
+    assert growth_placement(0, 100, 4) == [(0, 0)] * 4
+    assert growth_placement(250, 100, 4) == [(0, 100), (100, 200), (200, 250), (250, 250)]
+    assert growth_placement(400, 100, 4)[-1] == (300, 400)
+    with pytest.raises(ValueError):
+        growth_placement(401, 100, 4)
+    # the placement is a contiguous partition of [0, n) for every n (exact merge, I1)
+    for n in range(0, 401, 7):
+        rs = growth_placement(n, 100, 4)
+        assert rs[0][0] == 0 and rs[-1][1] == n
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(3))
