@@ -306,3 +306,42 @@ def test_error_codes(M):
     q = torch.zeros((1, 32, 128), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(M.MedhaError, match="ENOTSUP"):
         M.attn_decode_partial([sh], q, [0])   # G = 32
+
+
+def test_decode_step_host_single_gpu(M):
+    """The end-to-end C-ABI call (host buffers in, host buffers out) equals the device
+    path: append the new token, decode it, copy o/lse back."""
+    N, h_kv, G, d = 30000, 8, 4, 128
+    k, v = make_global_kv(91, N, h_kv, d)
+    q = synth.queries(91, 1, h_kv * G, d, amp=6.0)
+    sh = to_shard(k, v, 0, N - 1, extra_cap=5)
+    ws = M.decode_step_workspace(1, h_kv * G, h_kv, d)
+    o_h = torch.empty((h_kv * G, d), dtype=torch.float32).pin_memory()
+    l_h = torch.empty((h_kv * G,), dtype=torch.float32).pin_memory()
+    M.decode_step_host(None, sh, True, q[0].contiguous().pin_memory(), k[N - 1].contiguous().pin_memory(),
+                       v[N - 1].contiguous().pin_memory(), N - 1, o_h, l_h, ws)
+    torch.cuda.synchronize()
+    assert sh.len == N
+    o, l = M.attn_decode_partial([sh], q.cuda(), [N - 1])
+    assert torch.equal(o[0].cpu(), o_h) and torch.equal(l[0].cpu(), l_h)
+    ro, rl = oracle_attention(q, k, v, [N - 1])
+    compare(o_h[None], l_h[None], ro, rl, what="decode_step_host")
+
+
+def test_abi_argument_errors(M):
+    import ctypes
+    lib = M.lib
+    assert lib.medha_kvp_decode(None, None, 1, None, 32, None, 1.0, None, None, None, None, 0, None) == -1
+    assert lib.medha_merge_partials(None, 2, 4, 128, None, None, None, None) == -1
+    parts = torch.zeros((2, 4 * 129), device="cuda")
+    o = torch.zeros((4, 128), device="cuda")
+    assert lib.medha_merge_partials(ctypes.c_void_p(parts.data_ptr()), 65, 4, 128, ctypes.c_void_p(o.data_ptr()),
+                                    None, None, None) == -1          # P > 64
+    assert lib.medha_merge_partials(ctypes.c_void_p(parts.data_ptr()), 2, 4, 96, ctypes.c_void_p(o.data_ptr()),
+                                    None, None, None) == -4          # d = 96
+    sh = M.KVShard.empty(1, 8, 64)
+    with pytest.raises(M.MedhaError, match="EWORKSPACE"):
+        M.attn_decode_partial([sh], torch.zeros((1, 4, 64), dtype=torch.bfloat16, device="cuda"), [0],
+                              ws=torch.zeros(16, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(M.MedhaError, match="ENOTSUP"):
+        M.attn_prefill_chunk(sh, torch.zeros((70000, 4, 64), dtype=torch.bfloat16, device="cuda"), 0)
