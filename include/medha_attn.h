@@ -128,6 +128,26 @@ medha_status medha_attn_prefill_chunk(const medha_kv_shard *kv, const void *q, i
                                       void *stream);
 
 /*
+ * attn_prefill_batch (prefill-prefill batching): n chunks of
+ * different sequences of the same layer (same h_q, h_kv, d; each chunk over its own shard
+ * and its own query block), computed in ONE launch per 32 chunks with a batch-wide
+ * balanced split plan; per chunk the result equals medha_attn_prefill_chunk.
+ *   chunks_host: host array of n descriptors, read during the call.
+ *   Workspace: medha_prefill_batch_workspace_size(n, c of every chunk, h_q, d) bytes.
+ */
+typedef struct medha_prefill_chunk {
+  const medha_kv_shard *kv;   /* host pointer to the chunk's shard */
+  const void *q;              /* device, bf16 [c][h_q][d] */
+  int64_t c;                  /* query tokens (1 .. 65536) */
+  int64_t q_pos0;             /* absolute position of query token 0 */
+  float *o;                   /* device, fp32 [c][h_q][d] */
+  float *lse;                 /* device, fp32 [c][h_q], natural log */
+} medha_prefill_chunk;
+size_t medha_prefill_batch_workspace_size(int32_t n, const int64_t *c_host, int32_t h_q, int32_t d);
+medha_status medha_attn_prefill_batch(const medha_prefill_chunk *chunks_host, int32_t n, int32_t h_q,
+                                      float scale, void *ws, size_t ws_bytes, void *stream);
+
+/*
  * merge_partials: parts is fp32 [P][rows*(d+1)] where part r
  * holds o_r [rows][d] followed by lse_r [rows].  Writes o_out fp32 [rows][d],
  * lse_out fp32 [rows] (may be NULL) and o_out_bf16 bf16 [rows][d] (may be NULL).

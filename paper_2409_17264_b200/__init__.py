@@ -217,6 +217,43 @@ def attn_prefill_chunk(shard: KVShard, q: torch.Tensor, q_pos0: int, scale=None,
     return o, lse
 
 
+class _PrefillChunk(ctypes.Structure):
+    _fields_ = [("kv", ctypes.POINTER(_Shard)), ("q", ctypes.c_void_p), ("c", ctypes.c_int64),
+                ("q_pos0", ctypes.c_int64), ("o", ctypes.c_void_p), ("lse", ctypes.c_void_p)]
+
+
+_sig("medha_prefill_batch_workspace_size", _sz, _i32, _P(_i64), _i32, _i32)
+_sig("medha_attn_prefill_batch", _i32, _P(_PrefillChunk), _i32, _i32, _f32, _vp, _sz, _vp)
+
+
+def attn_prefill_batch(shards: Sequence[KVShard], qs: Sequence[torch.Tensor], q_pos0s: Sequence[int], scale=None,
+                       ws=None, stream=None):
+    """Prefill-prefill batching: chunk i (bf16 [c_i][h_q][d]) at positions
+    q_pos0s[i].. over shards[i], all chunks in one launch.  Returns [(o_i, lse_i)]."""
+    n = len(shards)
+    if len(qs) != n or len(q_pos0s) != n:
+        raise ValueError("need one shard, one query block and one q_pos0 per chunk")
+    h_q, d = qs[0].shape[1], qs[0].shape[2]
+    outs = []
+    arr = (_PrefillChunk * n)()
+    keep = []
+    for i, (sh, q, p0) in enumerate(zip(shards, qs, q_pos0s)):
+        _need_cuda(q, f"q[{i}]", torch.bfloat16)
+        c = q.shape[0]
+        o = torch.empty((c, h_q, d), dtype=torch.float32, device=q.device)
+        lse = torch.empty((c, h_q), dtype=torch.float32, device=q.device)
+        cs = sh.c()
+        keep.append(cs)
+        arr[i] = _PrefillChunk(ctypes.pointer(cs), q.data_ptr(), c, int(p0), o.data_ptr(), lse.data_ptr())
+        outs.append((o, lse))
+    if ws is None:
+        cs_arr = (ctypes.c_int64 * n)(*[q.shape[0] for q in qs])
+        ws = _workspace("prefill_batch", lib.medha_prefill_batch_workspace_size(n, cs_arr, h_q, d), qs[0].device)
+    _check(lib.medha_attn_prefill_batch(arr, n, h_q, _scale(scale, d), _ptr(ws), ws.numel(), _stream(stream)),
+           "attn_prefill_batch")
+    return outs
+
+
 def merge_partials(parts: torch.Tensor, rows: int, d: int, want_bf16: bool = False, stream=None):
     """K5: parts fp32 [P][rows*(d+1)] (o then lse per part) -> (o [rows][d], lse [rows], o_bf16|None)."""
     _need_cuda(parts, "parts", torch.float32)

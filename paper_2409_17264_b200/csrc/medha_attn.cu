@@ -290,75 +290,101 @@ medha_status make_map_3d(CUtensorMap *m, const void *base, uint64_t d0, uint64_t
   return MEDHA_OK;
 }
 
-struct PrefillPlan {
-  int m_pairs, n_split, tiles_per_split;
-  int64_t rows, part_stride;
-  size_t ws_bytes;
+// One chunk of a prefill batch (host side).
+struct PrefillChunk {
+  const medha_kv_shard *kv;
+  const void *q;
+  int64_t c, q_pos0;
+  float *o, *lse;
 };
 
-// Grid = (query-tile pairs) x (kv heads) x (KV splits).  The split count is chosen to
-// minimise an estimate of the makespan: waves x KV tiles per CTA (wave quantisation on
-// the SM count) plus the HBM time of writing and merging split partials.
-PrefillPlan plan_prefill(int64_t c, int32_t h_q, int32_t h_kv, int32_t d, int64_t n_kv_max) {
-  PrefillPlan pl;
-  const int G = h_kv > 0 ? std::max(1, h_q / h_kv) : 1;
+// Batch planner.  Every CTA processes one 2-tile query pair of one kv head over a range of
+// `T` KV tiles (the same T for the whole batch keeps CTA durations balanced); a chunk with
+// more KV tiles is split into cdiv(kv_tiles, T) ranges merged afterwards (K5).  T is chosen
+// to minimise an estimate of the makespan: waves on the SM count x T, plus the HBM time of
+// writing and merging split partials.
+struct PrefillBatchPlan {
+  std::vector<int> m_pairs, n_split, tps;
+  std::vector<int64_t> rows, part_stride;
+  std::vector<size_t> ws_off;
+  size_t ws_bytes = 0;
+  int64_t n_items = 0;
+};
+
+PrefillBatchPlan plan_prefill_batch(const PrefillChunk *ch, int n, int32_t h_q, int32_t h_kv, int32_t d) {
+  PrefillBatchPlan pl;
+  const int G = std::max(1, h_q / std::max(1, h_kv));
   const int TQ = kWsTileM / std::max(1, std::min(G, kWsTileM));
-  pl.m_pairs = (int)cdiv(std::max<int64_t>(c, 1), 2 * TQ);
-  pl.rows = c * h_q;
-  pl.part_stride = (int64_t)round_up((size_t)(pl.rows * (d + 1)), 4);
-  const int64_t kv_tiles = std::max<int64_t>(1, cdiv(n_kv_max, kWsTileN));
-  const int64_t base = (int64_t)pl.m_pairs * h_kv;
+  std::vector<int64_t> kv_tiles(n);
+  int64_t max_tiles = 1;
+  for (int i = 0; i < n; ++i) {
+    pl.m_pairs.push_back((int)cdiv(std::max<int64_t>(ch[i].c, 1), 2 * TQ));
+    pl.rows.push_back(ch[i].c * h_q);
+    pl.part_stride.push_back((int64_t)round_up((size_t)(ch[i].c * h_q * (d + 1)), 4));
+    const medha_kv_shard *kv = ch[i].kv;
+    const int64_t n_kv = std::max<int64_t>(0, std::min<int64_t>(kv->len, ch[i].q_pos0 + ch[i].c - 1 - kv->pos0 + 1));
+    kv_tiles[i] = std::max<int64_t>(1, cdiv(n_kv, kWsTileN));
+    max_tiles = std::max(max_tiles, kv_tiles[i]);
+  }
   const int sms = num_sms();
-  const double t_tile_us = 1.2;                                   // ~2x1024 MMA clk per KV tile and pair
-  const double merge_us_per_split = (double)pl.rows * (d + 1) * 4 * 2 / 6.0e6;  // write + read at ~6 TB/s
+  const double t_tile_us = 1.2;   // ~2 x 1024 MMA clk per KV tile and query pair
   double best = 1e300;
-  int best_ns = 1;
+  int64_t best_T = max_tiles;
   for (int ns = 1; ns <= 64; ++ns) {
-    const int64_t tps = cdiv(kv_tiles, ns);
-    const int64_t ns_eff = cdiv(kv_tiles, tps);
-    if (ns_eff != ns) continue;
-    if (ns > 1 && tps < 4) break;
-    const int64_t waves = cdiv(base * ns, sms);
-    const double est = (double)waves * tps * t_tile_us + (ns > 1 ? merge_us_per_split * ns : 0.0);
+    const int64_t T = cdiv(max_tiles, ns);
+    if (ns > 1 && T < 4) break;
+    int64_t ctas = 0;
+    double merge_us = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const int64_t nsi = std::min<int64_t>(64, cdiv(kv_tiles[i], T));
+      ctas += (int64_t)pl.m_pairs[i] * h_kv * nsi;
+      if (nsi > 1) merge_us += (double)pl.rows[i] * (d + 1) * 4 * 2 * nsi / 6.0e6;
+    }
+    const double est = (double)cdiv(ctas, sms) * T * t_tile_us + merge_us;
     if (est < best * 0.999) {
       best = est;
-      best_ns = ns;
+      best_T = T;
     }
   }
-  pl.tiles_per_split = (int)cdiv(kv_tiles, best_ns);
-  pl.n_split = (int)cdiv(kv_tiles, pl.tiles_per_split);
-  pl.ws_bytes = pl.n_split > 1 ? (size_t)pl.n_split * pl.part_stride * sizeof(float) : 0;
+  for (int i = 0; i < n; ++i) {
+    int64_t nsi = std::min<int64_t>(64, cdiv(kv_tiles[i], best_T));
+    const int64_t tpsi = cdiv(kv_tiles[i], nsi);
+    nsi = cdiv(kv_tiles[i], tpsi);
+    pl.n_split.push_back((int)nsi);
+    pl.tps.push_back((int)tpsi);
+    pl.ws_off.push_back(pl.ws_bytes);
+    if (nsi > 1) pl.ws_bytes += round_up((size_t)nsi * pl.part_stride[i] * sizeof(float), 256);
+    pl.n_items += (int64_t)pl.m_pairs[i] * h_kv * nsi;
+  }
   return pl;
 }
 
 size_t prefill_ws_bound(int64_t c, int32_t h_q, int32_t d) {
   const int64_t rows = c * h_q;
-  return (size_t)64 * round_up((size_t)(rows * (d + 1)), 4) * sizeof(float) + 256;
+  return round_up((size_t)64 * round_up((size_t)(rows * (d + 1)), 4) * sizeof(float), 256);
 }
 
 template <int D, int G>
-medha_status launch_prefill(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv,
-                            const PrefillWsParams &p, dim3 grid, cudaStream_t st) {
+medha_status launch_prefill(const PrefillBatch &b, int64_t items, cudaStream_t st) {
   using L = WsLayout<D>;
   static bool attr_done = false;
   if (!attr_done) {
     CUDA_TRY(cudaFuncSetAttribute(prefill_ws_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kAlloc));
     attr_done = true;
   }
-  prefill_ws_kernel<D, G><<<grid, kWsThreads, L::kAlloc, st>>>(mq, mk, mv, p);
+  prefill_ws_kernel<D, G><<<(unsigned)items, kWsThreads, L::kAlloc, st>>>(b);
   LAUNCH_CHECK("prefill_ws_kernel");
   return MEDHA_OK;
 }
 
 template <int D>
-medha_status dispatch_prefill_g(int G, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv,
-                                const PrefillWsParams &p, dim3 grid, cudaStream_t st) {
+medha_status dispatch_prefill_g(int G, const PrefillBatch &b, int64_t items, cudaStream_t st) {
   switch (G) {
-    case 1: return launch_prefill<D, 1>(mq, mk, mv, p, grid, st);
-    case 2: return launch_prefill<D, 2>(mq, mk, mv, p, grid, st);
-    case 4: return launch_prefill<D, 4>(mq, mk, mv, p, grid, st);
-    case 8: return launch_prefill<D, 8>(mq, mk, mv, p, grid, st);
-    case 16: return launch_prefill<D, 16>(mq, mk, mv, p, grid, st);
+    case 1: return launch_prefill<D, 1>(b, items, st);
+    case 2: return launch_prefill<D, 2>(b, items, st);
+    case 4: return launch_prefill<D, 4>(b, items, st);
+    case 8: return launch_prefill<D, 8>(b, items, st);
+    case 16: return launch_prefill<D, 16>(b, items, st);
     default: return fail(MEDHA_ENOTSUP, "group size %d", G);
   }
 }
@@ -379,55 +405,93 @@ medha_status merge_impl(const float *parts, int32_t P, int64_t rows, int64_t par
   return MEDHA_OK;
 }
 
+// A batch of up to kPfMaxBatch prefill chunks (all of the same layer: h_q, h_kv, d) in
+// one launch, then one K5 merge per chunk whose KV range was split.
+medha_status prefill_batch_impl(const PrefillChunk *ch, int n, int32_t h_q, float scale, void *ws, size_t ws_bytes,
+                                cudaStream_t st) {
+  if (n <= 0) return n == 0 ? MEDHA_OK : fail(MEDHA_EINVAL, "negative batch");
+  if (!(scale > 0.f)) return fail(MEDHA_EINVAL, "scale must be > 0");
+  medha_status s;
+  const int32_t h_kv = ch[0].kv ? ch[0].kv->h_kv : 0, d = ch[0].kv ? ch[0].kv->d : 0;
+  for (int i = 0; i < n; ++i) {
+    if ((s = check_shard(ch[i].kv))) return s;
+    if (ch[i].kv->h_kv != h_kv || ch[i].kv->d != d) return fail(MEDHA_ESHAPE, "chunks disagree on h_kv/d");
+    if (ch[i].c < 1) return fail(MEDHA_EINVAL, "chunk %d is empty", i);
+    if (ch[i].c > 65536) return fail(MEDHA_ENOTSUP, "chunk %lld > 65536", (long long)ch[i].c);
+    if (!ch[i].q || !ch[i].o || !ch[i].lse) return fail(MEDHA_EINVAL, "null argument (chunk %d)", i);
+    if (!aligned16(ch[i].q) || !aligned16(ch[i].o)) return fail(MEDHA_EINVAL, "q/o not 16-byte aligned");
+    if (ch[i].kv->capacity > INT32_MAX) return fail(MEDHA_ENOTSUP, "capacity > 2^31 tokens");
+  }
+  if (h_q <= 0 || h_q % h_kv != 0) return fail(MEDHA_EINVAL, "h_q %d not a multiple of h_kv %d", h_q, h_kv);
+  const int G = h_q / h_kv;
+  if (!supported_g(G)) return fail(MEDHA_ENOTSUP, "group size %d not in {1,2,4,8,16}", G);
+  size_t ws_used = 0;
+  for (int b0 = 0; b0 < n; b0 += kPfMaxBatch) {
+    const int nb = std::min(kPfMaxBatch, n - b0);
+    PrefillBatchPlan pl = plan_prefill_batch(ch + b0, nb, h_q, h_kv, d);
+    if (pl.ws_bytes > 0) {
+      if (!ws || !aligned16(ws)) return fail(MEDHA_EWORKSPACE, "null/misaligned workspace");
+      if (ws_used + pl.ws_bytes > ws_bytes)
+        return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, ws_used + pl.ws_bytes);
+    }
+    if (pl.n_items > INT32_MAX) return fail(MEDHA_ERANGE, "grid too large");
+    thread_local PrefillBatch b;   // ~15 KB of kernel parameters (host-side staging, per thread)
+    memset(&b, 0, sizeof(b));
+    b.n_seq = nb;
+    const int TQ = kWsTileM / G;
+    int64_t item = 0;
+    for (int i = 0; i < nb; ++i) {
+      const PrefillChunk &c = ch[b0 + i];
+      const medha_kv_shard *kv = c.kv;
+      if ((s = make_map_3d(&b.maps[i][0], c.q, d, h_q, c.c, (uint64_t)d * 2, (uint64_t)h_q * d * 2, 64, G, TQ)))
+        return s;
+      const uint64_t len_ext = (uint64_t)std::max<int64_t>(kv->len, 1);
+      if ((s = make_map_3d(&b.maps[i][1], kv->k, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64,
+                           kWsTileN, 1)))
+        return s;
+      if ((s = make_map_3d(&b.maps[i][2], kv->v, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64,
+                           kWsTileN, 1)))
+        return s;
+      PrefillWsParams &p = b.seq[i];
+      const bool split = pl.n_split[i] > 1;
+      p.o = split ? reinterpret_cast<float *>(static_cast<char *>(ws) + ws_used + pl.ws_off[i]) : c.o;
+      p.lse = c.lse;
+      p.c = c.c;
+      p.len = kv->len;
+      p.pos0 = kv->pos0;
+      p.q_pos0 = c.q_pos0;
+      p.rows = pl.rows[i];
+      p.part_stride = pl.part_stride[i];
+      p.h_q = h_q;
+      p.h_kv = h_kv;
+      p.n_split = pl.n_split[i];
+      p.tiles_per_split = pl.tps[i];
+      p.m_pairs = pl.m_pairs[i];
+      p.item_begin = (int32_t)item;
+      p.scale_log2 = scale * kLog2e;
+      item += (int64_t)pl.m_pairs[i] * h_kv * pl.n_split[i];
+    }
+    s = (d == 128) ? dispatch_prefill_g<128>(G, b, item, st) : dispatch_prefill_g<64>(G, b, item, st);
+    if (s) return s;
+    for (int i = 0; i < nb; ++i) {
+      if (pl.n_split[i] <= 1) continue;
+      const PrefillChunk &c = ch[b0 + i];
+      s = merge_impl(b.seq[i].o, pl.n_split[i], pl.rows[i], pl.part_stride[i], d, c.o, c.lse, nullptr, st);
+      if (s) return s;
+    }
+    ws_used += pl.ws_bytes;
+  }
+  return MEDHA_OK;
+}
+
 medha_status prefill_impl(const medha_kv_shard *kv, const void *q, int64_t c, int32_t h_q, int64_t q_pos0,
                           float scale, float *o, float *lse, void *ws, size_t ws_bytes, cudaStream_t st) {
   medha_status s = check_shard(kv);
   if (s) return s;
   if (c < 0) return fail(MEDHA_EINVAL, "negative chunk");
   if (c == 0) return MEDHA_OK;
-  if (c > 65536) return fail(MEDHA_ENOTSUP, "chunk %lld > 65536", (long long)c);
-  if (!q || !o || !lse) return fail(MEDHA_EINVAL, "null argument");
-  if (!aligned16(q) || !aligned16(o)) return fail(MEDHA_EINVAL, "q/o not 16-byte aligned");
-  if (!(scale > 0.f)) return fail(MEDHA_EINVAL, "scale must be > 0");
-  const int32_t h_kv = kv->h_kv, d = kv->d;
-  if (h_q <= 0 || h_q % h_kv != 0) return fail(MEDHA_EINVAL, "h_q %d not a multiple of h_kv %d", h_q, h_kv);
-  const int G = h_q / h_kv;
-  if (!supported_g(G)) return fail(MEDHA_ENOTSUP, "group size %d not in {1,2,4,8,16}", G);
-  if (kv->capacity > INT32_MAX) return fail(MEDHA_ENOTSUP, "capacity > 2^31 tokens");
-  const int64_t n_kv_max = std::max<int64_t>(0, std::min<int64_t>(kv->len, q_pos0 + c - 1 - kv->pos0 + 1));
-  PrefillPlan pl = plan_prefill(c, h_q, h_kv, d, n_kv_max);
-  if (pl.n_split > 1) {
-    if (!ws || !aligned16(ws)) return fail(MEDHA_EWORKSPACE, "null/misaligned workspace");
-    if (ws_bytes < pl.ws_bytes) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, pl.ws_bytes);
-  }
-  CUtensorMap mq, mk, mv;
-  const int TQ = kWsTileM / G;
-  if ((s = make_map_3d(&mq, q, d, h_q, c, (uint64_t)d * 2, (uint64_t)h_q * d * 2, 64, G, TQ))) return s;
-  const uint64_t len_ext = (uint64_t)std::max<int64_t>(kv->len, 1);
-  if ((s = make_map_3d(&mk, kv->k, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64, kWsTileN, 1)))
-    return s;
-  if ((s = make_map_3d(&mv, kv->v, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64, kWsTileN, 1)))
-    return s;
-  PrefillWsParams p;
-  memset(&p, 0, sizeof(p));
-  p.o = pl.n_split > 1 ? static_cast<float *>(ws) : o;
-  p.lse = lse;
-  p.c = c;
-  p.len = kv->len;
-  p.pos0 = kv->pos0;
-  p.q_pos0 = q_pos0;
-  p.rows = pl.rows;
-  p.part_stride = pl.part_stride;
-  p.h_q = h_q;
-  p.h_kv = h_kv;
-  p.n_split = pl.n_split;
-  p.tiles_per_split = pl.tiles_per_split;
-  p.scale_log2 = scale * kLog2e;
-  dim3 grid(pl.m_pairs, h_kv, pl.n_split);
-  s = (d == 128) ? dispatch_prefill_g<128>(G, mq, mk, mv, p, grid, st) : dispatch_prefill_g<64>(G, mq, mk, mv, p, grid, st);
-  if (s) return s;
-  if (pl.n_split > 1) return merge_impl(static_cast<float *>(ws), pl.n_split, pl.rows, pl.part_stride, d, o, lse, nullptr, st);
-  return MEDHA_OK;
+  PrefillChunk one{kv, q, c, q_pos0, o, lse};
+  return prefill_batch_impl(&one, 1, h_q, scale, ws, ws_bytes, st);
 }
 
 }  // namespace
@@ -598,6 +662,26 @@ size_t medha_prefill_workspace_size(int64_t c, int32_t h_q, int32_t h_kv, int32_
 medha_status medha_attn_prefill_chunk(const medha_kv_shard *kv, const void *q, int64_t c, int32_t h_q, int64_t q_pos0,
                                       float scale, float *o, float *lse, void *ws, size_t ws_bytes, void *stream) {
   return prefill_impl(kv, q, c, h_q, q_pos0, scale, o, lse, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t medha_prefill_batch_workspace_size(int32_t n, const int64_t *c_host, int32_t h_q, int32_t d) {
+  if (n <= 0 || !c_host || h_q <= 0 || d <= 0) return 256;
+  size_t total = 0;
+  for (int i = 0; i < n; ++i) total += prefill_ws_bound(std::max<int64_t>(c_host[i], 1), h_q, d);
+  return total;
+}
+
+medha_status medha_attn_prefill_batch(const medha_prefill_chunk *chunks_host, int32_t n, int32_t h_q, float scale,
+                                      void *ws, size_t ws_bytes, void *stream) {
+  if (n < 0) return fail(MEDHA_EINVAL, "negative batch");
+  if (n == 0) return MEDHA_OK;
+  if (!chunks_host) return fail(MEDHA_EINVAL, "null chunk array");
+  std::vector<PrefillChunk> ch(n);
+  for (int i = 0; i < n; ++i) {
+    const medha_prefill_chunk &c = chunks_host[i];
+    ch[i] = PrefillChunk{c.kv, c.q, c.c, c.q_pos0, c.o, c.lse};
+  }
+  return prefill_batch_impl(ch.data(), n, h_q, scale, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 medha_status medha_merge_partials(const float *parts, int32_t P, int64_t rows, int32_t d, float *o_out, float *lse_out,

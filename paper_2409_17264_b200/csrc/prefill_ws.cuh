@@ -65,7 +65,19 @@ struct PrefillWsParams {
   int32_t h_kv;
   int32_t n_split;
   int32_t tiles_per_split;
+  int32_t m_pairs;      // 2-tile query pairs of this chunk
+  int32_t item_begin;   // first CTA of this chunk in the batch grid
   float scale_log2;
+};
+
+// A batch of prefill chunks, each over its own shard, in ONE launch (prefill-prefill
+// batching).  CTA items of chunk s are [item_begin, next item_begin), ordered
+// pair-fastest, then kv head, then KV split (concurrent CTAs share K/V tiles through L2).
+constexpr int kPfMaxBatch = 32;
+struct PrefillBatch {
+  CUtensorMap maps[kPfMaxBatch][3];   // Q, K, V per chunk
+  PrefillWsParams seq[kPfMaxBatch];
+  int32_t n_seq;
 };
 
 template <int D>
@@ -187,8 +199,7 @@ __device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[12
 
 template <int D, int G>
 __global__ void __launch_bounds__(kWsThreads, 1)
-    prefill_ws_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ PrefillWsParams p) {
+    prefill_ws_kernel(const __grid_constant__ PrefillBatch batch) {
   static_assert(D == 64 || D == 128, "D");
   static_assert(kWsTileM % G == 0, "G");
   using L = WsLayout<D>;
@@ -211,7 +222,16 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
-  const int pair = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
+  int sq = 0;
+  while (sq + 1 < batch.n_seq && (int)blockIdx.x >= batch.seq[sq + 1].item_begin) ++sq;
+  const PrefillWsParams &p = batch.seq[sq];
+  const CUtensorMap *tmq = &batch.maps[sq][0];
+  const CUtensorMap *tmk = &batch.maps[sq][1];
+  const CUtensorMap *tmv = &batch.maps[sq][2];
+  const int local = (int)blockIdx.x - p.item_begin;
+  const int pair = local % p.m_pairs;
+  const int kvh = (local / p.m_pairs) % p.h_kv;
+  const int split = local / (p.m_pairs * p.h_kv);
   const int64_t t0 = (int64_t)pair * 2 * TQ;                 // first query token of tile A
   const int64_t t1 = min64(p.c, t0 + 2 * TQ);
   const int64_t n_kv = max64(0, min64(p.len, p.q_pos0 + t1 - 1 - p.pos0 + 1));
@@ -251,21 +271,21 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   if (warp == 0) {
     // ================================ TMA producer ================================
     if (lane == 0 && n > 0) {
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
+      tma_prefetch_desc(tmq);
+      tma_prefetch_desc(tmk);
+      tma_prefetch_desc(tmv);
       mbar_arrive_expect_tx(bar_q, 2 * L::kQBytes);
 #pragma unroll
       for (int x = 0; x < 2; ++x)
 #pragma unroll
         for (int hh = 0; hh < NH; ++hh)
-          tma_load_3d(sQ + x * L::kQBytes + hh * L::kHalf, &tm_q, bar_q, 64 * hh, kvh * G, (int32_t)(t0 + x * TQ));
+          tma_load_3d(sQ + x * L::kQBytes + hh * L::kHalf, tmq, bar_q, 64 * hh, kvh * G, (int32_t)(t0 + x * TQ));
       for (int it = 0; it < 2 * n; ++it) {
         const int s = it % kWsSlots;
         if (it >= kWsSlots) mbar_wait(bar_empty + s, ((it / kWsSlots) - 1) & 1);
         mbar_arrive_expect_tx(bar_full + s, L::kSlotBytes);
         const int32_t tok = (jt0 + (it >> 1)) * kWsTileN;
-        const void *map = (it & 1) ? (const void *)&tm_v : (const void *)&tm_k;
+        const void *map = (it & 1) ? (const void *)tmv : (const void *)tmk;
 #pragma unroll
         for (int hh = 0; hh < NH; ++hh) tma_load_3d(slot_ptr(s) + hh * L::kHalf, map, bar_full + s, 64 * hh, tok, kvh);
       }

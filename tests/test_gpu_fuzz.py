@@ -40,6 +40,40 @@ def test_fuzz_decode(M, case):
         compare(o[b:b + 1], lse[b:b + 1], refs[b][0], refs[b][1], what=f"fuzz decode {case}/{b}")
 
 
+@pytest.mark.parametrize("case", range(6))
+def test_prefill_batch_ppb(M, case):
+    """Prefill-prefill batching: chunks of different sequences
+    (ragged c, prefixes, shard offsets) in one launch equal the per-chunk calls and the
+    oracle."""
+    import torch
+    rng = np.random.default_rng(5000 + case)
+    d = int(rng.choice([64, 128]))
+    G = int(rng.choice([1, 4, 8]))
+    h_kv = int(rng.choice([1, 2]))
+    n = int(rng.integers(2, 9)) if case < 5 else 40            # last case: > 32 chunks (2 launches)
+    shards, qs, p0s, refs = [], [], [], []
+    for i in range(n):
+        c = int(rng.integers(1, 300))
+        P0 = int(rng.integers(0, 5000 if case < 5 else 800))
+        N = P0 + c
+        a = int(rng.integers(0, min(N, P0 + 1)))
+        k, v = make_global_kv(6000 + 100 * case + i, N, h_kv, d)
+        q = synth.queries(6000 + 100 * case + i, c, h_kv * G, d, amp=4.0, t0=P0)
+        shards.append(to_shard(k, v, a, N))
+        qs.append(q.cuda())
+        p0s.append(P0)
+        rows = sorted(set([0, c - 1, c // 2]))
+        refs.append((rows, oracle_attention(q[rows], k, v, [P0 + r for r in rows], (a, N))))
+    outs = M.attn_prefill_batch(shards, qs, p0s)
+    for i in range(n):
+        o, lse = outs[i]
+        rows, (ro, rl) = refs[i]
+        compare(o[rows], lse[rows], ro, rl, what=f"ppb {case}/{i}")
+        o1, l1 = M.attn_prefill_chunk(shards[i], qs[i], p0s[i])
+        # same kernel; only the batch-wide split plan can differ (fp32 summation order)
+        assert (o1 - o).abs().max().item() < 1e-4 and (l1 - lse).abs().max().item() < 1e-4
+
+
 @pytest.mark.parametrize("case", range(16))
 def test_fuzz_prefill(M, case):
     rng = np.random.default_rng(3000 + case)
