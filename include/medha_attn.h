@@ -75,13 +75,27 @@ int32_t medha_version(void);
  * sits at absolute position pos0 + j; tokens j >= len are never read.
  */
 typedef struct medha_kv_shard {
-  void *k;            /* device, bf16 [h_kv][capacity][d] */
-  void *v;            /* device, bf16 [h_kv][capacity][d] */
-  int64_t capacity;   /* tokens allocated per head */
+  void *k;            /* device, bf16 [h_kv][capacity][d] (paged: the page pool, see below) */
+  void *v;            /* device, bf16 [h_kv][capacity][d] (paged: the page pool) */
+  int64_t capacity;   /* logical tokens per head */
   int64_t len;        /* tokens valid per head (0 <= len <= capacity) */
   int64_t pos0;       /* absolute position of local token 0 */
   int32_t h_kv;       /* KV heads */
   int32_t d;          /* head dimension */
+  /* Paged KV: when page_table != NULL, k and v are page pools bf16
+   * [h_kv][pool_tokens][d] shared by many sequences, and logical token j of this shard lives
+   * at pool row page_table[j / page_size] * page_size + j % page_size.  capacity must be a
+   * multiple of page_size (page_table has capacity / page_size entries, device int32).
+   * page_size: power of two, >= 16 for decode/append, >= 128 for prefill.  Pool rows past
+   * len inside a shard's last page must hold finite values (zero-fill pools on allocation):
+   * the prefill's PV MMA reads whole 128-token tiles.  Table entries are not range-checked on
+ * the device: each must name a page inside the pool (pool_tokens / page_size pages) that no
+ * other live shard writes.  page_table == NULL: contiguous shard,
+   * page_size / pool_tokens ignored. */
+  const int32_t *page_table;
+  int32_t page_size;
+  int32_t reserved;   /* 0 */
+  int64_t pool_tokens; /* tokens per head plane of the pools (paged only) */
 } medha_kv_shard;
 
 /*

@@ -35,7 +35,8 @@ lib = ctypes.CDLL(LIB_PATH)
 class _Shard(ctypes.Structure):
     _fields_ = [("k", ctypes.c_void_p), ("v", ctypes.c_void_p), ("capacity", ctypes.c_int64),
                 ("len", ctypes.c_int64), ("pos0", ctypes.c_int64), ("h_kv", ctypes.c_int32),
-                ("d", ctypes.c_int32)]
+                ("d", ctypes.c_int32), ("page_table", ctypes.c_void_p), ("page_size", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("pool_tokens", ctypes.c_int64)]
 
 
 _vp, _i32, _i64, _f32, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
@@ -111,6 +112,9 @@ class KVShard:
     """One KVP shard of one sequence: bf16 k, v [h_kv][capacity][d] on the GPU.
 
     Local token j holds absolute position pos0 + j; `len` tokens are valid.
+    Paged: `KVShard.paged(pool_k, pool_v, page_table, page_size)` — k, v are
+    page pools [h_kv][pool_tokens][d] shared by many shards and local token j lives at pool
+    row page_table[j // page_size] * page_size + j % page_size (include/medha_attn.h).
     """
 
     def __init__(self, k: torch.Tensor, v: torch.Tensor, length: int = 0, pos0: int = 0):
@@ -122,6 +126,7 @@ class KVShard:
         self.h_kv, self.capacity, self.d = k.shape
         self.len = int(length)
         self.pos0 = int(pos0)
+        self.page_table, self.page_size, self.pool_tokens = None, 0, 0
 
     @classmethod
     def empty(cls, h_kv: int, capacity: int, d: int, pos0: int = 0, device=None):
@@ -129,8 +134,19 @@ class KVShard:
         v = torch.empty_like(k)
         return cls(k, v, 0, pos0)
 
+    @classmethod
+    def paged(cls, pool_k: torch.Tensor, pool_v: torch.Tensor, page_table: torch.Tensor, page_size: int,
+              length: int = 0, pos0: int = 0):
+        sh = cls(pool_k, pool_v, length, pos0)
+        _need_cuda(page_table, "page_table", torch.int32)
+        sh.page_table, sh.page_size, sh.pool_tokens = page_table, int(page_size), sh.capacity
+        sh.capacity = page_table.numel() * int(page_size)
+        return sh
+
     def c(self) -> _Shard:
-        return _Shard(self.k.data_ptr(), self.v.data_ptr(), self.capacity, self.len, self.pos0, self.h_kv, self.d)
+        pt = self.page_table
+        return _Shard(self.k.data_ptr(), self.v.data_ptr(), self.capacity, self.len, self.pos0, self.h_kv, self.d,
+                      None if pt is None else pt.data_ptr(), self.page_size, 0, self.pool_tokens)
 
 
 def _shards_c(shards: Sequence[KVShard]):

@@ -62,7 +62,9 @@ constexpr int kDecodeThreads = kDecodeWarps * 32;
 struct DecodeSeq {
   const __nv_bfloat16 *k;  // [h_kv][cap][D]
   const __nv_bfloat16 *v;
-  int64_t cap;
+  int64_t hstride;        // tokens between head planes (capacity, or pool_tokens when paged)
+  const int32_t *pt;      // page table (paged KV) or null
+  int32_t psl;            // log2(page size)
   int64_t n_vis;         // visible local tokens (keys 0..n_vis-1)
   int32_t split_tokens;  // tokens per split, multiple of 64
   int32_t n_splits;      // splits per kv head
@@ -147,8 +149,15 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   const int64_t t_begin = (int64_t)split * S.split_tokens;
   const int64_t t_end = min64(t_begin + S.split_tokens, S.n_vis);
 
-  const __nv_bfloat16 *kbase = S.k + (int64_t)kvh * S.cap * D;
-  const __nv_bfloat16 *vbase = S.v + (int64_t)kvh * S.cap * D;
+  const __nv_bfloat16 *kbase = S.k + (int64_t)kvh * S.hstride * D;
+  const __nv_bfloat16 *vbase = S.v + (int64_t)kvh * S.hstride * D;
+  // pool row of logical tile start tb (16-aligned; a page holds >= 16 tokens, so all 16
+  // tokens of a tile sit in one page); the page table is tiny and L1-resident
+  const int32_t *pt = S.pt;
+  const int psl = S.psl;
+  auto tile_row = [&](int64_t tb) -> int64_t {
+    return pt ? (((int64_t)__ldg(pt + (tb >> psl)) << psl) | (tb & ((1ll << psl) - 1))) : tb;
+  };
 
   // ---- Q fragments (rows g / g+8 = heads of this group), permuted like K ------------
   uint32_t qlo[KS][2], qhi[KS][2];
@@ -171,11 +180,12 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   float l_lo = 0.f, l_hi = 0.f;              // thread-partial running sums
 
   auto load_tile = [&](int64_t tb, uint4 (&kk)[2][KCH], uint4 (&vv)[4][VCH]) {
+    const int64_t row0 = tile_row(tb);
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       const int64_t tok = tb + 8 * n + g;
       const bool ok = tok < t_end;
-      const __nv_bfloat16 *src = kbase + tok * D + 8 * c;
+      const __nv_bfloat16 *src = kbase + (row0 + 8 * n + g) * D + 8 * c;
 #pragma unroll
       for (int i = 0; i < KCH; ++i) kk[n][i] = ok ? ldg_stream(src + 32 * i) : make_uint4(0, 0, 0, 0);
     }
@@ -183,7 +193,7 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
     for (int r = 0; r < 4; ++r) {
       const int64_t tok = tb + 2 * c + (r & 1) + 8 * (r >> 1);
       const bool ok = tok < t_end;
-      const __nv_bfloat16 *src = vbase + tok * D + 8 * g;
+      const __nv_bfloat16 *src = vbase + (row0 + 2 * c + (r & 1) + 8 * (r >> 1)) * D + 8 * g;
 #pragma unroll
       for (int i = 0; i < VCH; ++i) vv[r][i] = ok ? ldg_stream(src + 64 * i) : make_uint4(0, 0, 0, 0);
     }

@@ -80,8 +80,27 @@ medha_status check_shard(const medha_kv_shard *kv) {
   if (kv->len > kv->capacity) return fail(MEDHA_ERANGE, "shard len %lld > capacity %lld", (long long)kv->len,
                                           (long long)kv->capacity);
   if (!supported_d(kv->d)) return fail(MEDHA_ENOTSUP, "head dim %d not in {64,128}", kv->d);
+  if (kv->page_table) {
+    const int32_t ps = kv->page_size;
+    if (ps < 16 || (ps & (ps - 1))) return fail(MEDHA_EINVAL, "page_size %d not a power of two >= 16", ps);
+    if (kv->capacity % ps) return fail(MEDHA_EINVAL, "capacity %lld not a multiple of page_size %d",
+                                       (long long)kv->capacity, ps);
+    if (kv->pool_tokens < ps || kv->pool_tokens % ps)
+      return fail(MEDHA_EINVAL, "pool_tokens %lld not a positive multiple of page_size %d", (long long)kv->pool_tokens,
+                  ps);
+    if ((uintptr_t)kv->page_table & 3)
+      return fail(MEDHA_EINVAL, "page_table not 4-byte aligned");
+  }
   return MEDHA_OK;
 }
+
+int32_t log2_pow2(int32_t x) {
+  int32_t l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+// tokens between the head planes of a shard's K/V arrays
+int64_t head_stride(const medha_kv_shard &kv) { return kv.page_table ? kv.pool_tokens : kv.capacity; }
 
 // ---------------------------------------------------------------------------------------------
 // decode
@@ -238,7 +257,9 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
       DecodeSeq &S = p.seq[i];
       S.k = static_cast<const __nv_bfloat16 *>(kv.k);
       S.v = static_cast<const __nv_bfloat16 *>(kv.v);
-      S.cap = kv.capacity;
+      S.hstride = head_stride(kv);
+      S.pt = kv.page_table;
+      S.psl = kv.page_table ? log2_pow2(kv.page_size) : 0;
       S.n_vis = nvis[i];
       S.split_tokens = (int32_t)split_tokens;
       S.n_splits = (int32_t)ns;
@@ -420,7 +441,9 @@ medha_status prefill_batch_impl(const PrefillChunk *ch, int n, int32_t h_q, floa
     if (ch[i].c > 65536) return fail(MEDHA_ENOTSUP, "chunk %lld > 65536", (long long)ch[i].c);
     if (!ch[i].q || !ch[i].o || !ch[i].lse) return fail(MEDHA_EINVAL, "null argument (chunk %d)", i);
     if (!aligned16(ch[i].q) || !aligned16(ch[i].o)) return fail(MEDHA_EINVAL, "q/o not 16-byte aligned");
-    if (ch[i].kv->capacity > INT32_MAX) return fail(MEDHA_ENOTSUP, "capacity > 2^31 tokens");
+    if (head_stride(*ch[i].kv) > INT32_MAX) return fail(MEDHA_ENOTSUP, "capacity/pool > 2^31 tokens");
+    if (ch[i].kv->page_table && ch[i].kv->page_size < kWsTileN)
+      return fail(MEDHA_ENOTSUP, "prefill needs page_size >= %d (got %d)", kWsTileN, ch[i].kv->page_size);
   }
   if (h_q <= 0 || h_q % h_kv != 0) return fail(MEDHA_EINVAL, "h_q %d not a multiple of h_kv %d", h_q, h_kv);
   const int G = h_q / h_kv;
@@ -445,12 +468,14 @@ medha_status prefill_batch_impl(const PrefillChunk *ch, int n, int32_t h_q, floa
       const medha_kv_shard *kv = c.kv;
       if ((s = make_map_3d(&b.maps[i][0], c.q, d, h_q, c.c, (uint64_t)d * 2, (uint64_t)h_q * d * 2, 64, G, TQ)))
         return s;
-      const uint64_t len_ext = (uint64_t)std::max<int64_t>(kv->len, 1);
-      if ((s = make_map_3d(&b.maps[i][1], kv->k, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64,
-                           kWsTileN, 1)))
+      // contiguous: the map ends at len (TMA zero-fills the ragged tail); paged: the map
+      // spans the whole pool and the producer translates each 128-token tile through the
+      // page table (rows past len inside the last page are finite by contract, masked to 0)
+      const uint64_t hs = (uint64_t)head_stride(*kv);
+      const uint64_t len_ext = kv->page_table ? hs : (uint64_t)std::max<int64_t>(kv->len, 1);
+      if ((s = make_map_3d(&b.maps[i][1], kv->k, d, len_ext, h_kv, (uint64_t)d * 2, hs * d * 2, 64, kWsTileN, 1)))
         return s;
-      if ((s = make_map_3d(&b.maps[i][2], kv->v, d, len_ext, h_kv, (uint64_t)d * 2, (uint64_t)kv->capacity * d * 2, 64,
-                           kWsTileN, 1)))
+      if ((s = make_map_3d(&b.maps[i][2], kv->v, d, len_ext, h_kv, (uint64_t)d * 2, hs * d * 2, 64, kWsTileN, 1)))
         return s;
       PrefillWsParams &p = b.seq[i];
       const bool split = pl.n_split[i] > 1;
@@ -467,6 +492,8 @@ medha_status prefill_batch_impl(const PrefillChunk *ch, int n, int32_t h_q, floa
       p.n_split = pl.n_split[i];
       p.tiles_per_split = pl.tps[i];
       p.m_pairs = pl.m_pairs[i];
+      p.pt = kv->page_table;
+      p.psl = kv->page_table ? log2_pow2(kv->page_size) : 0;
       p.item_begin = (int32_t)item;
       p.scale_log2 = scale * kLog2e;
       item += (int64_t)pl.m_pairs[i] * h_kv * pl.n_split[i];
@@ -635,7 +662,8 @@ medha_status medha_kv_append(medha_kv_shard *kv, const void *k_new, const void *
   const int64_t blocks = std::min<int64_t>(cdiv(total, threads), (int64_t)num_sms() * 8);
   kv_append_kernel<<<(unsigned)blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint4 *>(k_new), static_cast<const uint4 *>(v_new), static_cast<uint4 *>(kv->k),
-      static_cast<uint4 *>(kv->v), n, kv->h_kv, vec, kv->capacity, kv->len);
+      static_cast<uint4 *>(kv->v), n, kv->h_kv, vec, head_stride(*kv), kv->len, kv->page_table,
+      kv->page_table ? log2_pow2(kv->page_size) : 0);
   LAUNCH_CHECK("kv_append_kernel");
   kv->len += n;
   return MEDHA_OK;

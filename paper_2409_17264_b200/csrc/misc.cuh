@@ -5,17 +5,21 @@
 namespace medha {
 
 // K1: scatter n new token-major rows [n][h_kv][D] into the
-// head-major shard [h_kv][cap][D] at local token `len`.  One 16-byte vector per thread.
+// head-major shard [h_kv][hstride][D] at local token `len` (through the page table when
+// the shard is paged).  One 16-byte vector per thread.
 __global__ void kv_append_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
                                  uint4 *__restrict__ k, uint4 *__restrict__ v, int64_t n, int32_t h_kv,
-                                 int32_t vec_per_row, int64_t cap, int64_t len) {
+                                 int32_t vec_per_row, int64_t hstride, int64_t len,
+                                 const int32_t *__restrict__ pt, int32_t psl) {
   const int64_t total = n * h_kv * vec_per_row;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / vec_per_row;          // row = t*h_kv + h
     const int32_t e = (int32_t)(i - row * vec_per_row);
     const int64_t t = row / h_kv;
     const int32_t h = (int32_t)(row - t * h_kv);
-    const int64_t dst = ((int64_t)h * cap + len + t) * vec_per_row + e;
+    int64_t j = len + t;                      // logical token; pool row when paged
+    if (pt) j = ((int64_t)pt[j >> psl] << psl) | (j & ((1ll << psl) - 1));
+    const int64_t dst = ((int64_t)h * hstride + j) * vec_per_row + e;
     k[dst] = k_new[i];
     v[dst] = v_new[i];
   }

@@ -65,6 +65,8 @@ struct PrefillWsParams {
   int32_t h_kv;
   int32_t n_split;
   int32_t tiles_per_split;
+  const int32_t *pt;    // page table (paged KV) or null; the K/V maps then span the pools
+  int32_t psl;          // log2(page size), >= 7 when paged
   int32_t m_pairs;      // 2-tile query pairs of this chunk
   int32_t item_begin;   // first CTA of this chunk in the batch grid
   float scale_log2;
@@ -284,7 +286,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         const int s = it % kWsSlots;
         if (it >= kWsSlots) mbar_wait(bar_empty + s, ((it / kWsSlots) - 1) & 1);
         mbar_arrive_expect_tx(bar_full + s, L::kSlotBytes);
-        const int32_t tok = (jt0 + (it >> 1)) * kWsTileN;
+        int32_t tok = (jt0 + (it >> 1)) * kWsTileN;   // logical tile start; pool row when paged
+        if (p.pt) tok = (__ldg(p.pt + (tok >> p.psl)) << p.psl) | (tok & ((1 << p.psl) - 1));
         const void *map = (it & 1) ? (const void *)tmv : (const void *)tmk;
 #pragma unroll
         for (int hh = 0; hh < NH; ++hh) tma_load_3d(slot_ptr(s) + hh * L::kHalf, map, bar_full + s, 64 * hh, tok, kvh);

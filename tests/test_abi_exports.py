@@ -53,3 +53,19 @@ def test_kernels_are_sm100a_and_use_tcgen05_tma():
     assert "UTMALDG" in sass
     assert "LDTM" in sass
     assert "HMMA" in sass  # decode dot products
+
+
+def test_shard_struct_layout_matches_binding(tmp_path):
+    """The ctypes mirror of medha_kv_shard (incl. the paged-KV fields) has the header's
+    size and field offsets, as compiled by the C compiler."""
+    from paper_2409_17264_b200 import _Shard
+    fields = [f for f, _ in _Shard._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "medha_attn.h"\nint main(void){\n'
+                   + 'printf("%zu\\n", sizeof(medha_kv_shard));\n'
+                   + "".join(f'printf("%zu\\n", offsetof(medha_kv_shard, {f}));\n' for f in fields) + "return 0;}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got[0] == ctypes.sizeof(_Shard)
+    assert got[1:] == [getattr(_Shard, f).offset for f in fields]
