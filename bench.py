@@ -123,9 +123,13 @@ def _max_over_ranks(x: float, world: int) -> float:
 def build_shard(M, rank, world, n_total, h_kv, d, extra_cap=0, seed=SEED):
     """Rank r holds global tokens [r n/P, (r+1) n/P), generated on the GPU by
     the counter-based generator (same global KV for every P)."""
+    return build_range(M, n_total * rank // world, n_total * (rank + 1) // world, h_kv, d, extra_cap, seed)
+
+
+def build_range(M, a, b, h_kv, d, extra_cap=0, seed=SEED):
+    """Shard holding global tokens [a, b) of the synthetic sequence `seed` (pos0 = a)."""
     import torch
     import synth
-    a, b = n_total * rank // world, n_total * (rank + 1) // world
     n = b - a
     sh = M.KVShard.empty(h_kv, n + extra_cap, d, pos0=a)
     blk = synth.BLOCK_TOKENS
@@ -323,6 +327,91 @@ def bench_70b_decode(M, iters=5, warm=2):
     return res
 
 
+def bench_mixed(M, rank, world, iters=5, warm=3):
+    """configs[4], the mixed hybrid batch under KVP = 4: per rank, one 512-token prefill chunk
+    of a 2M-context request over the rank's 512K-token slice (the tail rank also holds the
+    chunk's own K/V, Eq. 6) plus 8 rank-local short decodes over 4K-token KVs
+    (32 in all).  At N = 4 the step is measured as it runs (KVP prefill with
+    all-gather + merge, then the batched decodes), max over ranks.  At N = 1 every rank's
+    work is timed on this GPU in turn and the K5 merge of the four partials beside it; the
+    projected KVP = 4 step is the slowest rank + the merge (the exchange, 8 MiB per rank, is
+    measured only at N = 4)."""
+    import torch
+    import synth
+    from paper_2409_17264_b200 import accounting as acc
+    from paper_2409_17264_b200.kvp import shard_range
+    P, c, P0, n_short = 4, 512, 1 << 21, 4096
+    if world not in (1, P):
+        return None
+    comm = M.KVPComm() if world == P else None
+    q = synth.queries(SEED + 11, c, H_Q, D, device="cuda", amp=1.0, t0=P0)
+    rows = c * H_Q
+    pws = M.prefill_workspace(c, H_Q, H_KV, D)
+    dws = M.decode_workspace(8, H_Q, H_KV, D)
+    parts = torch.empty((P, rows * (D + 1)), dtype=torch.float32, device="cuda")
+    od = torch.empty((8, H_Q, D), dtype=torch.float32, device="cuda")
+    ld = torch.empty((8, H_Q), dtype=torch.float32, device="cuda")
+    per_rank = []
+    for r in ([rank] if comm is not None else range(P)):
+        a, b = shard_range(P0, r, P)
+        if r == P - 1:
+            b = P0 + c
+        sh = build_range(M, a, b, H_KV, D, seed=SEED + 11)
+        shorts = [build_range(M, 0, n_short, H_KV, D, seed=SEED + 100 + 8 * r + i) for i in range(8)]
+        qd = synth.queries(SEED + 100 + 8 * r, 8, H_Q, D, device="cuda", amp=4.0)
+        po, pl = parts[r, :rows * D].view(c, H_Q, D), parts[r, rows * D:].view(c, H_Q)
+
+        def step():
+            if comm is not None:
+                M.kvp_prefill_chunk(comm, sh, q, P0)
+            else:
+                M.attn_prefill_chunk(sh, q, P0, o=po, lse=pl, ws=pws)
+            M.attn_decode_partial(shorts, qd, [n_short - 1] * 8, o=od, lse=ld, ws=dws)
+
+        for _ in range(warm):
+            step()
+        _barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        _barrier(world)
+        per_rank.append(e0.elapsed_time(e1) / iters)
+        del sh, shorts
+        torch.cuda.empty_cache()
+    fl = acc.prefill_chunk_flops(c, P0, H_Q, D)
+    _, tf_peak, _, _ = _peaks()
+    roof_ms = fl / P / (tf_peak * 1e12) * 1e3
+    res = {"workload": "configs[4]: 32 x 4K-token decodes (8 per rank) + one c=512 chunk at 2M prefix, KVP=4",
+           "chunk_tflop": round(fl / 1e12, 3), "short_decode_bytes": acc.decode_bytes(32 * n_short, H_KV, D),
+           "rank_roofline_ms": round(roof_ms, 4)}
+    if comm is not None:
+        ms = _max_over_ranks(per_rank[0], world)
+        comm.close()
+        res.update({"measured": "N=4, max over ranks", "ms_per_step": round(ms, 4),
+                    "chunk_tflops": round(fl / (ms * 1e-3) / 1e12, 1), "frac_of_rank_roofline": round(roof_ms / ms, 4)})
+    else:
+        for _ in range(warm):
+            M.merge_partials(parts, rows, D)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            M.merge_partials(parts, rows, D)
+        e1.record()
+        torch.cuda.synchronize()
+        merge_ms = e0.elapsed_time(e1) / iters
+        ms = max(per_rank) + merge_ms
+        res.update({"measured": "N=1: each rank's work in turn on one GPU", "rank_ms": [round(x, 4) for x in per_rank],
+                    "merge_ms": round(merge_ms, 4), "kvp4_projected_ms_excl_exchange": round(ms, 4),
+                    "chunk_tflops_projected": round(fl / (ms * 1e-3) / 1e12, 1),
+                    "frac_of_rank_roofline": round(roof_ms / ms, 4)})
+    return res
+
+
 def hbm_probe(M, nbytes=4 << 30, iters=5):
     import torch
     buf = torch.empty(nbytes // 2, dtype=torch.bfloat16, device="cuda")
@@ -439,6 +528,10 @@ def main():
         del sh_p
         torch.cuda.empty_cache()
         extra["decode_70b_10M"] = bench_70b_decode(M)
+    if world in (1, 4) and not args.no_extra:
+        mixed = bench_mixed(M, rank, world)
+        if rank == 0:
+            extra["mixed_c4"] = mixed
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, s = cpu_oracle_sample(2, N_KV)

@@ -126,7 +126,9 @@ struct __align__(16) DecodeSmem {
 };
 
 // One work item: split `split` of kv head `kvh` of sequence `sidx`.
-template <int D, int G>
+// kPaged: some sequence of the launch has a page table (a separate instantiation keeps the
+// contiguous path's register allocation untouched)
+template <int D, int G, bool kPaged>
 __device__ __forceinline__ void decode_item(const DecodeParams &p, const int item, DecodeSmem<D, G> &sm) {
   constexpr int KCH = D / 32;   // 16-byte K chunks per lane per token
   constexpr int VCH = D / 64;   // 16-byte V chunks per lane per token
@@ -156,7 +158,9 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   const int32_t *pt = S.pt;
   const int psl = S.psl;
   auto tile_row = [&](int64_t tb) -> int64_t {
-    return pt ? (((int64_t)__ldg(pt + (tb >> psl)) << psl) | (tb & ((1ll << psl) - 1))) : tb;
+    if constexpr (kPaged)
+      return pt ? (((int64_t)__ldg(pt + (tb >> psl)) << psl) | (tb & ((1ll << psl) - 1))) : tb;
+    return tb;
   };
 
   // ---- Q fragments (rows g / g+8 = heads of this group), permuted like K ------------
@@ -534,7 +538,7 @@ __device__ __forceinline__ void xchg_merge_unit(const DecodeParams &p, const int
   __syncthreads();
 }
 
-template <int D, int G>
+template <int D, int G, bool kPaged>
 __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const __grid_constant__ DecodeParams p) {
   static_assert(D == 64 || D == 128, "D");
   static_assert(G >= 1 && G <= 16, "G");
@@ -547,7 +551,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     const int item = sm.item;
     __syncthreads();
     if (item >= p.n_items) break;
-    decode_item<D, G>(p, item, sm);
+    decode_item<D, G, kPaged>(p, item, sm);
     __syncthreads();
   }
   // fused KVP exchange: units are merged after this CTA's items (no CTA ever spins while

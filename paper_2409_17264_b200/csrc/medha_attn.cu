@@ -147,7 +147,12 @@ size_t decode_ws_layout(int32_t batch, int32_t h_q, int32_t h_kv, int32_t d, cha
 
 template <int D, int G>
 void launch_decode(const DecodeParams &p, int grid, cudaStream_t st) {
-  decode_splitkv_kernel<D, G><<<grid, kDecodeThreads, 0, st>>>(p);
+  bool paged = false;
+  for (int i = 0; i < p.n_seq; ++i) paged |= p.seq[i].pt != nullptr;
+  if (paged)
+    decode_splitkv_kernel<D, G, true><<<grid, kDecodeThreads, 0, st>>>(p);
+  else
+    decode_splitkv_kernel<D, G, false><<<grid, kDecodeThreads, 0, st>>>(p);
 }
 
 template <int D>
