@@ -42,6 +42,12 @@ __device__ unsigned long long g_decode_trace[8192][8];   // indexed by work item
       unsigned long long t_;                                                               \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
       g_decode_trace[item][k] = t_;                                                        \
+      if (k == 0) {                                                                        \
+        unsigned smid_;                                                                    \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                                \
+        g_decode_trace[item][4] = blockIdx.x;                                              \
+        g_decode_trace[item][5] = smid_;                                                   \
+      }                                                                                    \
     }                                                                                      \
   } while (0)
 #else

@@ -34,7 +34,12 @@ namespace medha {
 constexpr int kWsThreads = 384;
 constexpr int kWsTileM = 128;
 constexpr int kWsTileN = 128;
-constexpr int kWsSlots = 4;
+#ifndef MEDHA_PF_SLOTS128
+#define MEDHA_PF_SLOTS128 4     // K/V ring slots at d = 128 (32 KiB each; 5 fit in 227 KiB)
+#endif
+#ifndef MEDHA_PF_SLOTS64
+#define MEDHA_PF_SLOTS64 4      // K/V ring slots at d = 64 (16 KiB each)
+#endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef MEDHA_PF_SETMAXNREG
 #define MEDHA_PF_SETMAXNREG 0   // rebalance registers between warpgroups (A/B knob)
@@ -89,7 +94,9 @@ struct WsLayout {
   static constexpr uint32_t kSlotBytes = kWsTileN * D * 2;
   static constexpr uint32_t kQ0 = 0;
   static constexpr uint32_t kSlot0 = 2 * kQBytes;
-  static constexpr uint32_t kBar = kSlot0 + kWsSlots * kSlotBytes;
+  static constexpr int kSlots = D == 128 ? MEDHA_PF_SLOTS128 : MEDHA_PF_SLOTS64;
+  static_assert(kSlots >= 4 && kSlots <= 8, "slots");
+  static constexpr uint32_t kBar = kSlot0 + kSlots * kSlotBytes;
   static constexpr uint32_t kTotal = kBar + 256;
   static constexpr uint32_t kAlloc = kTotal + 1024;
 };
@@ -214,12 +221,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kBar);
   uint64_t *bar_q = bars + 0;
-  uint64_t *bar_full = bars + 1;              // [4]
-  uint64_t *bar_empty = bars + 5;             // [4]
-  uint64_t *bar_s = bars + 9;                 // [2]
-  uint64_t *bar_p = bars + 11;                // [2]
-  uint64_t *bar_o = bars + 13;                // [2]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 16);
+  constexpr int kWsSlots = L::kSlots;
+  uint64_t *bar_full = bars + 1;              // [kWsSlots]
+  uint64_t *bar_empty = bar_full + kWsSlots;  // [kWsSlots]
+  uint64_t *bar_s = bar_empty + kWsSlots;     // [2]
+  uint64_t *bar_p = bar_s + 2;                // [2]
+  uint64_t *bar_o = bar_p + 2;                // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_o + 2);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
