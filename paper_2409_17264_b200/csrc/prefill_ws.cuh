@@ -34,6 +34,9 @@ namespace medha {
 constexpr int kWsThreads = 384;
 constexpr int kWsTileM = 128;
 constexpr int kWsTileN = 128;
+#ifndef MEDHA_PF_ABLATE
+#define MEDHA_PF_ABLATE 0       // experiment-only ablations (1: skip the softmax)
+#endif
 #ifndef MEDHA_PF_SLOTS128
 #define MEDHA_PF_SLOTS128 4     // K/V ring slots at d = 128 (32 KiB each; 5 fit in 227 KiB)
 #endif
@@ -159,6 +162,8 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 // (i % MEDHA_PF_POLY_DEN) < MEDHA_PF_POLY_NUM evaluate exp2 with ex2_poly2 on the FMA pipe
 // (offloading the MUFU pipe, the softmax bottleneck: 128 ex2 per row per tile), the rest
 // with MUFU.EX2.
+constexpr uint32_t kPOff = 0;   // TMEM column of P inside its tile's S columns
+
 template <bool kMasked>
 __device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[128], float sl2, float mu,
                                              int nvalid) {
@@ -201,7 +206,7 @@ __device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[12
       add_bf16x2_f32(lsum2.x, lsum2.y, pk[e >> 1]);   // rounded P, one FHADD.BF16 per element
 #endif
     }
-    tmem_st16(tS + 16 * q, pk);
+    tmem_st16(tS + kPOff + 16 * q, pk);
   }
   return lsum2.x + lsum2.y;
 }
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         const uint32_t vb = smem_u32(slot_ptr(it % kWsSlots));
 #pragma unroll
         for (int ks = 0; ks < kWsTileN / 16; ++ks)
-          umma_f16_ts(tmem + 256 + x * 128, tmem + x * 128 + ks * 8, umma_desc_sw128(vb + ks * 2048, L::kHalf, 1024),
+          umma_f16_ts(tmem + 256 + x * 128, tmem + x * 128 + kPOff + ks * 8, umma_desc_sw128(vb + ks * 2048, L::kHalf, 1024),
                       kIdescO, (acc || ks > 0) ? 1u : 0u);
       };
       mbar_wait(bar_q, 0);
@@ -379,6 +384,14 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       mbar_wait(bar_s + x, j & 1);
       __syncwarp();
       tc_fence_after();
+#if MEDHA_PF_ABLATE == 1
+      // experiment only: no softmax (P = whatever S left) -- the MMA/TMA pipeline alone
+      tc_fence_before();
+      mbar_arrive(bar_p + x);
+      l_run = 1.f;
+      m_run = 0.f;
+      continue;
+#endif
       const int64_t jb = (int64_t)(jt0 + j) * kWsTileN;
       const bool full = (jb + kWsTileN - 1) <= j_lim_tile;
       const int nvalid = (int)min64(kWsTileN, max64(0, j_lim - jb + 1));   // valid cols [0, nvalid)
