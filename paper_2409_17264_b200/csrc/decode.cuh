@@ -550,6 +550,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
   static_assert(G >= 1 && G <= 16, "G");
   static_assert(kDecodeMaxSplits * G <= kDecodeSplitW || G > 8, "split weights");
   __shared__ DecodeSmem<D, G> sm;
+  // PDL: this grid's CTAs may be resident before the previous kernel on the stream ends;
+  // nothing is read or written before it has (KV rows, queue counters, outputs)
+  pdl_wait();
+  pdl_launch_dependents();
   // persistent: take work items from the queue until it runs dry
   for (;;) {
     if (threadIdx.x == 0) sm.item = (int)atomicAdd(p.work, 1u);

@@ -145,14 +145,33 @@ size_t decode_ws_layout(int32_t batch, int32_t h_q, int32_t h_kv, int32_t d, cha
   return off;
 }
 
+// Launch with programmatic dependent launch (PDL) allowed: the grid's CTAs take SMs as the
+// previous kernel's CTAs retire and start work (griddepcontrol.wait) the moment it
+// completes, instead of after a full launch latency.  MEDHA_PDL=0 turns it off.
+template <typename... Args>
+void launch_pdl(void (*kernel)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  static const bool on = getenv_flag("MEDHA_PDL", 1) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int D, int G>
 void launch_decode(const DecodeParams &p, int grid, cudaStream_t st) {
   bool paged = false;
   for (int i = 0; i < p.n_seq; ++i) paged |= p.seq[i].pt != nullptr;
   if (paged)
-    decode_splitkv_kernel<D, G, true><<<grid, kDecodeThreads, 0, st>>>(p);
+    launch_pdl(decode_splitkv_kernel<D, G, true>, dim3(grid), dim3(kDecodeThreads), 0, st, p);
   else
-    decode_splitkv_kernel<D, G, false><<<grid, kDecodeThreads, 0, st>>>(p);
+    launch_pdl(decode_splitkv_kernel<D, G, false>, dim3(grid), dim3(kDecodeThreads), 0, st, p);
 }
 
 template <int D>
@@ -665,10 +684,10 @@ medha_status medha_kv_append(medha_kv_shard *kv, const void *k_new, const void *
   const int64_t total = n * kv->h_kv * vec;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>(cdiv(total, threads), (int64_t)num_sms() * 8);
-  kv_append_kernel<<<(unsigned)blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint4 *>(k_new), static_cast<const uint4 *>(v_new), static_cast<uint4 *>(kv->k),
-      static_cast<uint4 *>(kv->v), n, kv->h_kv, vec, head_stride(*kv), kv->len, kv->page_table,
-      kv->page_table ? log2_pow2(kv->page_size) : 0);
+  launch_pdl(kv_append_kernel, dim3((unsigned)blocks), dim3(threads), 0, static_cast<cudaStream_t>(stream),
+             static_cast<const uint4 *>(k_new), static_cast<const uint4 *>(v_new), static_cast<uint4 *>(kv->k),
+             static_cast<uint4 *>(kv->v), (int64_t)n, kv->h_kv, vec, head_stride(*kv), kv->len,
+             (const int32_t *)kv->page_table, kv->page_table ? log2_pow2(kv->page_size) : 0);
   LAUNCH_CHECK("kv_append_kernel");
   kv->len += n;
   return MEDHA_OK;

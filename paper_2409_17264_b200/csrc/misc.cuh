@@ -11,6 +11,8 @@ __global__ void kv_append_kernel(const uint4 *__restrict__ k_new, const uint4 *_
                                  uint4 *__restrict__ k, uint4 *__restrict__ v, int64_t n, int32_t h_kv,
                                  int32_t vec_per_row, int64_t hstride, int64_t len,
                                  const int32_t *__restrict__ pt, int32_t psl) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t total = n * h_kv * vec_per_row;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / vec_per_row;          // row = t*h_kv + h
