@@ -417,7 +417,7 @@ medha_status launch_prefill(const PrefillBatch &b, int64_t items, cudaStream_t s
     CUDA_TRY(cudaFuncSetAttribute(prefill_ws_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kAlloc));
     attr_done = true;
   }
-  prefill_ws_kernel<D, G><<<(unsigned)items, kWsThreads, L::kAlloc, st>>>(b);
+  launch_pdl(prefill_ws_kernel<D, G>, dim3((unsigned)items), dim3(kWsThreads), (size_t)L::kAlloc, st, b);
   LAUNCH_CHECK("prefill_ws_kernel");
   return MEDHA_OK;
 }
@@ -440,12 +440,13 @@ medha_status merge_impl(const float *parts, int32_t P, int64_t rows, int64_t par
   const int warps_per_block = 8;
   const int64_t blocks = cdiv(rows, warps_per_block);
   if (blocks > INT32_MAX) return fail(MEDHA_ERANGE, "too many rows");
+  __nv_bfloat16 *ob = static_cast<__nv_bfloat16 *>(o_bf16);
   if (d == 128)
-    lse_merge_kernel<128><<<(unsigned)blocks, 32 * warps_per_block, 0, st>>>(parts, P, rows, part_stride, o_out, lse_out,
-                                                                            static_cast<__nv_bfloat16 *>(o_bf16));
+    launch_pdl(lse_merge_kernel<128>, dim3((unsigned)blocks), dim3(32 * warps_per_block), 0, st, parts, P, rows,
+               part_stride, o_out, lse_out, ob);
   else
-    lse_merge_kernel<64><<<(unsigned)blocks, 32 * warps_per_block, 0, st>>>(parts, P, rows, part_stride, o_out, lse_out,
-                                                                           static_cast<__nv_bfloat16 *>(o_bf16));
+    launch_pdl(lse_merge_kernel<64>, dim3((unsigned)blocks), dim3(32 * warps_per_block), 0, st, parts, P, rows,
+               part_stride, o_out, lse_out, ob);
   LAUNCH_CHECK("lse_merge_kernel");
   return MEDHA_OK;
 }

@@ -37,6 +37,8 @@ __global__ void lse_merge_kernel(const float *__restrict__ parts, int32_t P, int
                                  __nv_bfloat16 *__restrict__ o_bf16) {
   constexpr int PER = D / 32;  // floats per lane: d = lane + 32 i (coalesced; parts are packed, no alignment beyond 4 B)
   constexpr int U = 8;         // parts whose o rows are loaded together (latency hiding)
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;

@@ -221,6 +221,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   constexpr int NH = D / 64;
   constexpr uint32_t kIdescS = umma_idesc_bf16(kWsTileM, kWsTileN, 0);
   constexpr uint32_t kIdescO = umma_idesc_bf16(kWsTileM, D, 1);
+  pdl_wait();                 // PDL: the previous kernel on the stream (e.g. kv_append) is done
+  pdl_launch_dependents();    // the split merge may take SMs as this grid's last wave retires
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
