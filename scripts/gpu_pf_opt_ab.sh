@@ -12,6 +12,7 @@ for v in sys.argv[2:]:
     dmax = max((o[k][0] - base[k][0]).abs().max().item() for k in base)
     print(v, "bit-identical" if same else "DIFFERS", "max|dO| =", dmax)
 PY
+rm -f gpurun_out/pf_*.pt
 for v in "$@" $1; do
-  MEDHA_LIB_PATH=$PWD/$v timeout -s KILL 300 python scripts/prefill_sweep.py 131072,1048576 64,256,1024,4096 $(basename $v) 2>&1 | grep -v Warn
+  MEDHA_LIB_PATH=$PWD/$v timeout -s KILL 300 python scripts/prefill_sweep.py ${PF_PREFIXES:-131072,1048576} ${PF_CHUNKS:-64,256,1024,4096} $(basename $v) 2>&1 | grep -v Warn
 done
