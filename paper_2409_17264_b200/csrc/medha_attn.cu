@@ -980,6 +980,13 @@ medha_status medha_debug_decode_trace(unsigned long long *host_out /* [8192][8] 
 }
 #endif
 
+#ifdef MEDHA_PF_TRACE
+medha_status medha_debug_pf_trace(long long *host_out /* [512][12] */) {
+  CUDA_TRY(cudaMemcpyFromSymbol(host_out, g_pf_trace, sizeof(g_pf_trace)));
+  return MEDHA_OK;
+}
+#endif
+
 medha_status medha_hbm_read_probe(const void *src, size_t bytes, float *sink, void *stream) {
   if (!src || !sink) return fail(MEDHA_EINVAL, "null argument");
   if (!aligned16(src) || (bytes & 15)) return fail(MEDHA_EINVAL, "src/bytes not 16-byte aligned");

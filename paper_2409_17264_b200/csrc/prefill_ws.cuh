@@ -53,11 +53,28 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef MEDHA_PF_RAW_L
 #define MEDHA_PF_RAW_L 0   // normaliser: 0 rounded P via FHADD.BF16 (R20), 1 unrounded P, 2 rounded P via unpack
 #endif
+#ifndef MEDHA_PF_PSPLIT
+#define MEDHA_PF_PSPLIT 2   // P handed to the MMA warp in two key chunks: quarters [0, PSPLIT) and [PSPLIT, 4)
+#endif
+constexpr int kPChunks = 2;
 #ifndef MEDHA_PF_POLY_NUM      // fraction NUM/DEN of column pairs whose exp2 runs on the FMA pipe
 #define MEDHA_PF_POLY_NUM 0
 #endif
 #ifndef MEDHA_PF_POLY_DEN
 #define MEDHA_PF_POLY_DEN 3
+#endif
+
+#ifdef MEDHA_PF_TRACE
+// experiment only: clock64 stamps of the hand-offs in CTA 0, per KV tile (medha_debug_pf_trace)
+__device__ long long g_pf_trace[512][12];
+#define PF_STAMP(j, k)                                                  \
+  do {                                                                  \
+    if (blockIdx.x == 0 && (j) < 512) g_pf_trace[(j)][(k)] = clock64(); \
+  } while (0)
+#else
+#define PF_STAMP(j, k) \
+  do {                 \
+  } while (0)
 #endif
 
 struct PrefillWsParams {
@@ -166,7 +183,7 @@ constexpr uint32_t kPOff = 0;   // TMEM column of P inside its tile's S columns
 
 template <bool kMasked>
 __device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[128], float sl2, float mu,
-                                             int nvalid) {
+                                             int nvalid, uint64_t *bar_pc) {
   float2 lsum2 = make_float2(0.f, 0.f);
   const float2 sl2v = make_float2(sl2, sl2), nmu = make_float2(-mu, -mu);
   const float2 nmu384 = make_float2(-(384.f + mu), -(384.f + mu));   // exact: mu is an integer
@@ -207,6 +224,12 @@ __device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[12
 #endif
     }
     tmem_st16(tS + kPOff + 16 * q, pk);
+    if (q + 1 == MEDHA_PF_PSPLIT || q == 3) {
+      // key chunk complete: the MMA warp may start its share of O += P V
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar_pc + (q == 3 ? 1 : 0));
+    }
   }
   return lsum2.x + lsum2.y;
 }
@@ -232,8 +255,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   uint64_t *bar_full = bars + 1;              // [kWsSlots]
   uint64_t *bar_empty = bar_full + kWsSlots;  // [kWsSlots]
   uint64_t *bar_s = bar_empty + kWsSlots;     // [2]
-  uint64_t *bar_p = bar_s + 2;                // [2]
-  uint64_t *bar_o = bar_p + 2;                // [2]
+  uint64_t *bar_p = bar_s + 2;                // [2][kPChunks]
+  uint64_t *bar_o = bar_p + 2 * kPChunks;   // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_o + 2);
 
   const int tid = threadIdx.x;
@@ -264,7 +287,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     }
     for (int x = 0; x < 2; ++x) {
       mbar_init(bar_s + x, 1);
-      mbar_init(bar_p + x, 128);
+      for (int c = 0; c < kPChunks; ++c) mbar_init(bar_p + x * kPChunks + c, 128);
       mbar_init(bar_o + x, 1);
     }
     mbar_fence_init();
@@ -325,12 +348,21 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                       kIdescS, ks > 0);
         }
       };
-      auto issue_pv = [&](int x, int it, bool acc) {
+      // O_X += P_X V, key chunk by key chunk as the softmax hands P over
+      auto issue_pv = [&](int x, int it, bool acc, int j) {
         const uint32_t vb = smem_u32(slot_ptr(it % kWsSlots));
+        constexpr int kKsSplit = MEDHA_PF_PSPLIT * 2;   // two 16-key MMA steps per 32-key quarter
 #pragma unroll
-        for (int ks = 0; ks < kWsTileN / 16; ++ks)
-          umma_f16_ts(tmem + 256 + x * 128, tmem + x * 128 + kPOff + ks * 8, umma_desc_sw128(vb + ks * 2048, L::kHalf, 1024),
-                      kIdescO, (acc || ks > 0) ? 1u : 0u);
+        for (int c = 0; c < kPChunks; ++c) {
+          mbar_wait(bar_p + x * kPChunks + c, j & 1);
+          if (c == 0) PF_STAMP(j, 8 + x);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = c ? kKsSplit : 0; ks < (c ? kWsTileN / 16 : kKsSplit); ++ks) {
+            umma_f16_ts(tmem + 256 + x * 128, tmem + x * 128 + kPOff + ks * 8,
+                        umma_desc_sw128(vb + ks * 2048, L::kHalf, 1024), kIdescO, (acc || ks > 0) ? 1u : 0u);
+          }
+        }
       };
       mbar_wait(bar_q, 0);
       tc_fence_after();
@@ -343,18 +375,15 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       for (int j = 0; j < n; ++j) {
         const int iv = 2 * j + 1, ik = 2 * j + 2;
         wait_full(iv);
-        mbar_wait(bar_p + 0, j & 1);
-        tc_fence_after();
-        issue_pv(0, iv, j > 0);
+        issue_pv(0, iv, j > 0, j);
         if (j == n - 1) umma_commit(bar_o + 0);
         if (j + 1 < n) {
           wait_full(ik);
+          PF_STAMP(j, 10);
           issue_s(0, ik);
           umma_commit(bar_s + 0);
         }
-        mbar_wait(bar_p + 1, j & 1);
-        tc_fence_after();
-        issue_pv(1, iv, j > 0);
+        issue_pv(1, iv, j > 0, j);
         umma_commit(bar_empty + (iv % kWsSlots));
         if (j == n - 1) umma_commit(bar_o + 1);
         if (j + 1 < n) {
@@ -384,12 +413,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 
     for (int j = 0; j < n; ++j) {
       mbar_wait(bar_s + x, j & 1);
+      if ((warp & 3) == 0 && lane == 0) PF_STAMP(j, 4 * x + 0);
       __syncwarp();
       tc_fence_after();
 #if MEDHA_PF_ABLATE == 1
       // experiment only: no softmax (P = whatever S left) -- the MMA/TMA pipeline alone
       tc_fence_before();
-      mbar_arrive(bar_p + x);
+      for (int c = 0; c < kPChunks; ++c) mbar_arrive(bar_p + x * kPChunks + c);
       l_run = 1.f;
       m_run = 0.f;
       continue;
@@ -400,7 +430,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       // ---- row max (unmasked tiles take a compare-free path) ---------------------------
       uint32_t sreg[128];
       sm_load_row(tS, sreg);
+      if ((warp & 3) == 0 && lane == 0) PF_STAMP(j, 4 * x + 1);
       const float mx = full ? sm_rowmax<false>(sreg, nvalid) : sm_rowmax<true>(sreg, nvalid);
+#ifdef MEDHA_PF_TRACE
+      if ((warp & 3) == 0 && lane == 0 && blockIdx.x == 0 && j < 512) g_pf_trace[j][4 * x + 2] = clock64() + (mx > 1e30f);
+#endif
       const float m_tile = ceilf(mx * sl2);   // integer-valued (log2 units): exact rescales
       float m_use = m_run, alpha = 1.f;
       bool rescale = false;
@@ -411,25 +445,26 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       }
       m_run = m_use;
       const float mu = (m_use == -INFINITY) ? 0.f : m_use;
-      // ---- P = exp2(s*scale - m) -> bf16 -> TMEM (aliasing S) ------------------------
-      const float lsum = full ? sm_exp_pack<false>(tS, sreg, sl2, mu, nvalid)
-                              : sm_exp_pack<true>(tS, sreg, sl2, mu, nvalid);
-      // ---- O rescale (PV_X(j-1) is complete: covered by the S_X(j) commit) ----------
+      // ---- O rescale (PV_X(j-1) is complete: covered by the S_X(j) commit); it lands
+      // before the first P chunk is handed over (that hand-off waits for all TMEM stores)
       if (__any_sync(0xffffffffu, rescale)) {
-#pragma unroll
-        for (int q = 0; q < D / 32; ++q) {
-          uint32_t ro[32];
-          tmem_ld32(tO + 32 * q, ro);
+        // rare; 4 columns at a time (the S row is live in registers)
+#pragma unroll 1
+        for (int q = 0; q < D / 4; ++q) {
+          uint32_t ro[4];
+          tmem_ld4(tO + 4 * q, ro);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) ro[e] = __float_as_uint(__uint_as_float(ro[e]) * alpha);
-          tmem_st32(tO + 32 * q, ro);
+          for (int e = 0; e < 4; ++e) ro[e] = __float_as_uint(__uint_as_float(ro[e]) * alpha);
+          tmem_st4(tO + 4 * q, ro);
         }
       }
+      // ---- P = exp2(s*scale - m) -> bf16 -> TMEM (aliasing S), handed over in chunks ----
+      uint64_t *bar_pc = bar_p + x * kPChunks;
+      const float lsum = full ? sm_exp_pack<false>(tS, sreg, sl2, mu, nvalid, bar_pc)
+                              : sm_exp_pack<true>(tS, sreg, sl2, mu, nvalid, bar_pc);
+      if ((warp & 3) == 0 && lane == 0) PF_STAMP(j, 4 * x + 3);
       l_run = l_run * alpha + lsum;
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bar_p + x);
     }
 
     // ---- epilogue --------------------------------------------------------------------
