@@ -53,10 +53,8 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef MEDHA_PF_RAW_L
 #define MEDHA_PF_RAW_L 0   // normaliser: 0 rounded P via FHADD.BF16 (R20), 1 unrounded P, 2 rounded P via unpack
 #endif
-#ifndef MEDHA_PF_PSPLIT
-#define MEDHA_PF_PSPLIT 2   // P handed to the MMA warp in two key chunks: quarters [0, PSPLIT) and [PSPLIT, 4)
-#endif
-constexpr int kPChunks = 2;
+constexpr int kPChunks = 2;   // P handed to the MMA warp in two 64-key chunks
+
 #ifndef MEDHA_PF_POLY_NUM      // fraction NUM/DEN of column pairs whose exp2 runs on the FMA pipe
 #define MEDHA_PF_POLY_NUM 0
 #endif
@@ -71,7 +69,15 @@ __device__ long long g_pf_trace[512][12];
   do {                                                                  \
     if (blockIdx.x == 0 && (j) < 512) g_pf_trace[(j)][(k)] = clock64(); \
   } while (0)
+#define PF_STAMP_MAX(mx)                                                                         \
+  do {                                                                                           \
+    if ((warp & 3) == 0 && lane == 0 && blockIdx.x == 0 && j < 512)                              \
+      g_pf_trace[j][4 * x + 2] = clock64() + ((mx) > 1e30f);                                     \
+  } while (0)
 #else
+#define PF_STAMP_MAX(mx) \
+  do {                   \
+  } while (0)
 #define PF_STAMP(j, k) \
   do {                 \
   } while (0)
@@ -181,14 +187,14 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 // with MUFU.EX2.
 constexpr uint32_t kPOff = 0;   // TMEM column of P inside its tile's S columns
 
-template <bool kMasked>
-__device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[128], float sl2, float mu,
-                                             int nvalid, uint64_t *bar_pc) {
-  float2 lsum2 = make_float2(0.f, 0.f);
+// Quarters [Q0, Q1) of the row (32 columns each); the row sum accumulates into lsum2.
+template <bool kMasked, int Q0, int Q1>
+__device__ __forceinline__ void sm_exp_pack(uint32_t tS, const uint32_t (&s)[128], float sl2, float mu,
+                                            int nvalid, float2 &lsum2) {
   const float2 sl2v = make_float2(sl2, sl2), nmu = make_float2(-mu, -mu);
   const float2 nmu384 = make_float2(-(384.f + mu), -(384.f + mu));   // exact: mu is an integer
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = Q0; q < Q1; ++q) {
     uint32_t pk[16];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
@@ -224,14 +230,14 @@ __device__ __forceinline__ float sm_exp_pack(uint32_t tS, const uint32_t (&s)[12
 #endif
     }
     tmem_st16(tS + kPOff + 16 * q, pk);
-    if (q + 1 == MEDHA_PF_PSPLIT || q == 3) {
-      // key chunk complete: the MMA warp may start its share of O += P V
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bar_pc + (q == 3 ? 1 : 0));
-    }
   }
-  return lsum2.x + lsum2.y;
+}
+
+// hand a completed P chunk to the MMA warp (P stores, then O rescale stores, are visible)
+__device__ __forceinline__ void p_handoff(uint64_t *bar) {
+  tmem_wait_st();
+  tc_fence_before();
+  mbar_arrive(bar);
 }
 
 template <int D, int G>
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       // O_X += P_X V, key chunk by key chunk as the softmax hands P over
       auto issue_pv = [&](int x, int it, bool acc, int j) {
         const uint32_t vb = smem_u32(slot_ptr(it % kWsSlots));
-        constexpr int kKsSplit = MEDHA_PF_PSPLIT * 2;   // two 16-key MMA steps per 32-key quarter
+        constexpr int kKsSplit = kWsTileN / 16 / kPChunks;
 #pragma unroll
         for (int c = 0; c < kPChunks; ++c) {
           mbar_wait(bar_p + x * kPChunks + c, j & 1);
@@ -427,42 +433,53 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       const int64_t jb = (int64_t)(jt0 + j) * kWsTileN;
       const bool full = (jb + kWsTileN - 1) <= j_lim_tile;
       const int nvalid = (int)min64(kWsTileN, max64(0, j_lim - jb + 1));   // valid cols [0, nvalid)
-      // ---- row max (unmasked tiles take a compare-free path) ---------------------------
       uint32_t sreg[128];
       sm_load_row(tS, sreg);
       if ((warp & 3) == 0 && lane == 0) PF_STAMP(j, 4 * x + 1);
-      const float mx = full ? sm_rowmax<false>(sreg, nvalid) : sm_rowmax<true>(sreg, nvalid);
-#ifdef MEDHA_PF_TRACE
-      if ((warp & 3) == 0 && lane == 0 && blockIdx.x == 0 && j < 512) g_pf_trace[j][4 * x + 2] = clock64() + (mx > 1e30f);
-#endif
-      const float m_tile = ceilf(mx * sl2);   // integer-valued (log2 units): exact rescales
       float m_use = m_run, alpha = 1.f;
       bool rescale = false;
+      float2 lsum2 = make_float2(0.f, 0.f);
+      uint64_t *bar_pc = bar_p + x * kPChunks;
+      // O rescale (PV_X(j-1) is complete: covered by the S_X(j) commit); it lands before
+      // the first P chunk is handed over (the hand-off waits for all TMEM stores).  Rare;
+      // 4 columns at a time (the S row is live in registers).
+      auto rescale_o = [&]() {
+        if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll 1
+          for (int q = 0; q < D / 4; ++q) {
+            uint32_t ro[4];
+            tmem_ld4(tO + 4 * q, ro);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 4; ++e) ro[e] = __float_as_uint(__uint_as_float(ro[e]) * alpha);
+            tmem_st4(tO + 4 * q, ro);
+          }
+        }
+      };
+      // ---- row max (unmasked tiles take a compare-free path), then P ----------------
+      const float mx = full ? sm_rowmax<false>(sreg, nvalid) : sm_rowmax<true>(sreg, nvalid);
+      PF_STAMP_MAX(mx);
+      const float m_tile = ceilf(mx * sl2);   // integer-valued (log2 units): exact rescales
       if (m_tile > m_run + kRescaleThreshold || (m_run == -INFINITY && m_tile != -INFINITY)) {
         m_use = m_tile;
         alpha = exp2_int(m_run - m_tile);   // 0 when m_run = -inf
         rescale = (j > 0) && (m_run != -INFINITY);
       }
-      m_run = m_use;
+      rescale_o();
+      // ---- P = exp2(s*scale - m) -> bf16 -> TMEM (aliasing S), handed over in chunks --
       const float mu = (m_use == -INFINITY) ? 0.f : m_use;
-      // ---- O rescale (PV_X(j-1) is complete: covered by the S_X(j) commit); it lands
-      // before the first P chunk is handed over (that hand-off waits for all TMEM stores)
-      if (__any_sync(0xffffffffu, rescale)) {
-        // rare; 4 columns at a time (the S row is live in registers)
-#pragma unroll 1
-        for (int q = 0; q < D / 4; ++q) {
-          uint32_t ro[4];
-          tmem_ld4(tO + 4 * q, ro);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 4; ++e) ro[e] = __float_as_uint(__uint_as_float(ro[e]) * alpha);
-          tmem_st4(tO + 4 * q, ro);
-        }
+      if (full) {
+        sm_exp_pack<false, 0, 2>(tS, sreg, sl2, mu, nvalid, lsum2);
+        p_handoff(bar_pc + 0);
+        sm_exp_pack<false, 2, 4>(tS, sreg, sl2, mu, nvalid, lsum2);
+      } else {
+        sm_exp_pack<true, 0, 2>(tS, sreg, sl2, mu, nvalid, lsum2);
+        p_handoff(bar_pc + 0);
+        sm_exp_pack<true, 2, 4>(tS, sreg, sl2, mu, nvalid, lsum2);
       }
-      // ---- P = exp2(s*scale - m) -> bf16 -> TMEM (aliasing S), handed over in chunks ----
-      uint64_t *bar_pc = bar_p + x * kPChunks;
-      const float lsum = full ? sm_exp_pack<false>(tS, sreg, sl2, mu, nvalid, bar_pc)
-                              : sm_exp_pack<true>(tS, sreg, sl2, mu, nvalid, bar_pc);
+      p_handoff(bar_pc + 1);
+      m_run = m_use;
+      const float lsum = lsum2.x + lsum2.y;
       if ((warp & 3) == 0 && lane == 0) PF_STAMP(j, 4 * x + 3);
       l_run = l_run * alpha + lsum;
     }
