@@ -247,7 +247,13 @@ medha_status medha_kvp_prefill_chunk(medha_kvp_comm *comm, const medha_kv_shard 
  * appends the new token to `kv` (kv->len += 1), runs the decode attention at
  * position q_pos — locally when comm == NULL, otherwise as medha_kvp_decode — and
  * copies o (fp32 [h_q][d]) and lse (fp32 [h_q]) back into o_host / lse_host.
- * Asynchronous: the host buffers are valid after the stream is synchronised.
+ * Host buffers that are pinned AND mapped into the device address space (cudaHostAlloc
+ * under UVA, e.g. torch pin_memory(), 16-byte aligned) are accessed zero-copy: one
+ * kv_append launch reads q, k_new, v_new over the host link and the decode kernel writes
+ * o / lse straight into o_host / lse_host (no cudaMemcpyAsync); other host memory is
+ * staged with cudaMemcpyAsync.  Same bytes cross the link either way.
+ * Asynchronous: the host buffers are read/written while the stream executes the call
+ * and the outputs are valid after the stream is synchronised.
  */
 size_t medha_decode_step_workspace_size(int32_t world, int32_t h_q, int32_t h_kv, int32_t d);
 medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, int32_t append,

@@ -671,6 +671,38 @@ const char *medha_last_error(void) { return g_last_error.c_str(); }
 
 int32_t medha_version(void) { return (1 << 16) | 0; }
 
+namespace {
+// kv_append, optionally with a 16-byte-vector copy riding in the same launch (decode_step_host)
+medha_status kv_append_impl(medha_kv_shard *kv, const void *k_new, const void *v_new, int64_t n, const void *cp_src,
+                            void *cp_dst, int64_t cp_bytes, cudaStream_t st) {
+  const int32_t vec = kv->d / 8;
+  const int64_t total = std::max<int64_t>(n * kv->h_kv * vec, cp_bytes / 16);
+  const int threads = 256;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(total, threads), (int64_t)num_sms() * 8));
+  launch_pdl(kv_append_kernel, dim3((unsigned)blocks), dim3(threads), 0, st, static_cast<const uint4 *>(k_new),
+             static_cast<const uint4 *>(v_new), static_cast<uint4 *>(kv->k), static_cast<uint4 *>(kv->v), (int64_t)n,
+             kv->h_kv, vec, head_stride(*kv), kv->len, (const int32_t *)kv->page_table,
+             kv->page_table ? log2_pow2(kv->page_size) : 0, static_cast<const uint4 *>(cp_src),
+             static_cast<uint4 *>(cp_dst), cp_bytes / 16);
+  LAUNCH_CHECK("kv_append_kernel");
+  kv->len += n;
+  return MEDHA_OK;
+}
+
+// Device view of a host buffer: non-null iff it is pinned and mapped into the device's
+// address space (cudaHostAlloc memory under UVA, e.g. torch pin_memory()), so kernels can
+// read / write it directly over the host link (zero-copy).
+void *mapped_host_view(const void *h) {
+  if (!h) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
+}
+}  // namespace
+
 medha_status medha_kv_append(medha_kv_shard *kv, const void *k_new, const void *v_new, int64_t n, void *stream) {
   medha_status s = check_shard(kv);
   if (s) return s;
@@ -681,17 +713,7 @@ medha_status medha_kv_append(medha_kv_shard *kv, const void *k_new, const void *
   if (kv->len + n > kv->capacity)
     return fail(MEDHA_ERANGE, "append %lld tokens at len %lld exceeds capacity %lld", (long long)n, (long long)kv->len,
                 (long long)kv->capacity);
-  const int32_t vec = kv->d / 8;
-  const int64_t total = n * kv->h_kv * vec;
-  const int threads = 256;
-  const int64_t blocks = std::min<int64_t>(cdiv(total, threads), (int64_t)num_sms() * 8);
-  launch_pdl(kv_append_kernel, dim3((unsigned)blocks), dim3(threads), 0, static_cast<cudaStream_t>(stream),
-             static_cast<const uint4 *>(k_new), static_cast<const uint4 *>(v_new), static_cast<uint4 *>(kv->k),
-             static_cast<uint4 *>(kv->v), (int64_t)n, kv->h_kv, vec, head_stride(*kv), kv->len,
-             (const int32_t *)kv->page_table, kv->page_table ? log2_pow2(kv->page_size) : 0);
-  LAUNCH_CHECK("kv_append_kernel");
-  kv->len += n;
-  return MEDHA_OK;
+  return kv_append_impl(kv, k_new, v_new, n, nullptr, nullptr, 0, static_cast<cudaStream_t>(stream));
 }
 
 size_t medha_decode_workspace_size(int32_t batch, int32_t h_q, int32_t h_kv, int32_t d) {
@@ -956,20 +978,42 @@ medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, in
   float *lse_dev = reinterpret_cast<float *>(b);
   b += round_up((size_t)h_q * 4, 256);
   const size_t rest = ws_bytes - (size_t)(b - static_cast<char *>(ws));
-  CUDA_TRY(cudaMemcpyAsync(q_dev, q_host, qb, cudaMemcpyHostToDevice, st));
-  if (append) {
-    CUDA_TRY(cudaMemcpyAsync(k_dev, k_new_host, kb, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(v_dev, v_new_host, kb, cudaMemcpyHostToDevice, st));
-    if ((s = medha_kv_append(kv, k_dev, v_dev, 1, stream))) return s;
+  // Inputs: with mapped pinned host buffers, ONE launch reads q, k_new and v_new over the
+  // host link (q into the workspace, K/V appended straight into the shard); otherwise three
+  // cudaMemcpyAsync + kv_append.
+  const void *q_map = mapped_host_view(q_host);
+  const void *k_map = append ? mapped_host_view(k_new_host) : nullptr;
+  const void *v_map = append ? mapped_host_view(v_new_host) : nullptr;
+  const bool zc_in = q_map && aligned16(q_map) && (qb % 16 == 0) &&
+                     (!append || (k_map && v_map && aligned16(k_map) && aligned16(v_map)));
+  if (zc_in) {
+    if (append && kv->len + 1 > kv->capacity) return fail(MEDHA_ERANGE, "append exceeds capacity");
+    if ((s = kv_append_impl(kv, k_map, v_map, append ? 1 : 0, q_map, q_dev, (int64_t)qb, st))) return s;
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(q_dev, q_host, qb, cudaMemcpyHostToDevice, st));
+    if (append) {
+      CUDA_TRY(cudaMemcpyAsync(k_dev, k_new_host, kb, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(v_dev, v_new_host, kb, cudaMemcpyHostToDevice, st));
+      if ((s = medha_kv_append(kv, k_dev, v_dev, 1, stream))) return s;
+    }
   }
+  // Outputs: written by the decode kernel straight into mapped pinned host buffers
+  // (visible to the host once the stream is synchronised), else staged and copied back.
+  float *o_map = static_cast<float *>(mapped_host_view(o_host));
+  float *l_map = lse_host ? static_cast<float *>(mapped_host_view(lse_host)) : nullptr;
+  const bool zc_out = o_map && aligned16(o_map) && (!lse_host || l_map);
+  float *o_tgt = zc_out ? o_map : o_dev;
+  float *l_tgt = zc_out ? (lse_host ? l_map : lse_dev) : lse_dev;
   const int64_t qp = q_pos;
   if (comm)
-    s = medha_kvp_decode(comm, kv, 1, q_dev, h_q, &qp, scale, o_dev, lse_dev, nullptr, b, rest, stream);
+    s = medha_kvp_decode(comm, kv, 1, q_dev, h_q, &qp, scale, o_tgt, l_tgt, nullptr, b, rest, stream);
   else
-    s = decode_partial_impl(kv, 1, q_dev, h_q, &qp, scale, o_dev, lse_dev, b, rest, st);
+    s = decode_partial_impl(kv, 1, q_dev, h_q, &qp, scale, o_tgt, l_tgt, b, rest, st);
   if (s) return s;
-  CUDA_TRY(cudaMemcpyAsync(o_host, o_dev, (size_t)h_q * d * 4, cudaMemcpyDeviceToHost, st));
-  if (lse_host) CUDA_TRY(cudaMemcpyAsync(lse_host, lse_dev, (size_t)h_q * 4, cudaMemcpyDeviceToHost, st));
+  if (!zc_out) {
+    CUDA_TRY(cudaMemcpyAsync(o_host, o_dev, (size_t)h_q * d * 4, cudaMemcpyDeviceToHost, st));
+    if (lse_host) CUDA_TRY(cudaMemcpyAsync(lse_host, lse_dev, (size_t)h_q * 4, cudaMemcpyDeviceToHost, st));
+  }
   return MEDHA_OK;
 }
 

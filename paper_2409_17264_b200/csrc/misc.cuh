@@ -7,13 +7,18 @@ namespace medha {
 // K1: scatter n new token-major rows [n][h_kv][D] into the
 // head-major shard [h_kv][hstride][D] at local token `len` (through the page table when
 // the shard is paged).  One 16-byte vector per thread.
+// cp_n > 0 (decode_step_host): the same launch also copies cp_n 16-byte vectors cp_src -> cp_dst
+// (the step's query, read straight from mapped pinned host memory).
 __global__ void kv_append_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
                                  uint4 *__restrict__ k, uint4 *__restrict__ v, int64_t n, int32_t h_kv,
                                  int32_t vec_per_row, int64_t hstride, int64_t len,
-                                 const int32_t *__restrict__ pt, int32_t psl) {
+                                 const int32_t *__restrict__ pt, int32_t psl,
+                                 const uint4 *__restrict__ cp_src, uint4 *__restrict__ cp_dst, int64_t cp_n) {
   pdl_wait();
   pdl_launch_dependents();
   const int64_t total = n * h_kv * vec_per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cp_n; i += (int64_t)gridDim.x * blockDim.x)
+    cp_dst[i] = cp_src[i];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / vec_per_row;          // row = t*h_kv + h
     const int32_t e = (int32_t)(i - row * vec_per_row);
