@@ -50,6 +50,15 @@ __device__ unsigned long long g_decode_trace[8192][8];   // indexed by work item
       }                                                                                    \
     }                                                                                      \
   } while (0)
+// per launch (ring of 64): [0] CTA 0 resident, [1] CTA 0 past griddepcontrol.wait, [2] last
+// CTA out, [3] the preceding kv_append past its wait; g_ltrace_n counts traced launches
+__device__ unsigned long long g_ltrace[64][4];
+__device__ unsigned g_ltrace_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #else
 #define MEDHA_TRACE(k) do {} while (0)
 #endif
@@ -550,10 +559,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
   static_assert(G >= 1 && G <= 16, "G");
   static_assert(kDecodeMaxSplits * G <= kDecodeSplitW || G > 8, "split weights");
   __shared__ DecodeSmem<D, G> sm;
+#ifdef MEDHA_DECODE_TRACE
+  const unsigned long long t_entry = gtimer();
+#endif
   // PDL: this grid's CTAs may be resident before the previous kernel on the stream ends;
   // nothing is read or written before it has (KV rows, queue counters, outputs)
   pdl_wait();
   pdl_launch_dependents();
+#ifdef MEDHA_DECODE_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g_ltrace[g_ltrace_n & 63][0] = t_entry;
+    g_ltrace[g_ltrace_n & 63][1] = gtimer();
+  }
+#endif
   // persistent: take work items from the queue until it runs dry
   for (;;) {
     if (threadIdx.x == 0) sm.item = (int)atomicAdd(p.work, 1u);
@@ -574,6 +592,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     if (atomicAdd(p.work + 1, 1u) == gridDim.x - 1) {
       p.work[0] = 0u;
       p.work[1] = 0u;
+#ifdef MEDHA_DECODE_TRACE
+      g_ltrace[g_ltrace_n & 63][2] = gtimer();
+      g_ltrace_n = g_ltrace_n + 1;
+#endif
     }
   }
 }

@@ -1022,6 +1022,11 @@ medha_status medha_debug_decode_trace(unsigned long long *host_out /* [8192][8] 
   CUDA_TRY(cudaMemcpyFromSymbol(host_out, g_decode_trace, sizeof(g_decode_trace)));
   return MEDHA_OK;
 }
+medha_status medha_debug_launch_trace(unsigned long long *host_out /* [64][4] */, unsigned *n_out) {
+  CUDA_TRY(cudaMemcpyFromSymbol(host_out, g_ltrace, sizeof(g_ltrace)));
+  CUDA_TRY(cudaMemcpyFromSymbol(n_out, g_ltrace_n, sizeof(unsigned)));
+  return MEDHA_OK;
+}
 #endif
 
 #ifdef MEDHA_PF_TRACE

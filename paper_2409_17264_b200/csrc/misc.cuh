@@ -16,6 +16,9 @@ __global__ void kv_append_kernel(const uint4 *__restrict__ k_new, const uint4 *_
                                  const uint4 *__restrict__ cp_src, uint4 *__restrict__ cp_dst, int64_t cp_n) {
   pdl_wait();
   pdl_launch_dependents();
+#ifdef MEDHA_DECODE_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_ltrace[g_ltrace_n & 63][3] = gtimer();
+#endif
   const int64_t total = n * h_kv * vec_per_row;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cp_n; i += (int64_t)gridDim.x * blockDim.x)
     cp_dst[i] = cp_src[i];

@@ -15,7 +15,7 @@ import bench  # noqa: E402
 import synth  # noqa: E402
 import paper_2409_17264_b200 as M  # noqa: E402
 
-for n in (1 << 20, 1 << 18, 1 << 17):
+for n in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1048576,262144,131072").split(",")]:
     sh = bench.build_shard(M, 0, 1, n, 8, 128)
     q = synth.queries(1, 1, 32, 128, device="cuda", amp=4.0)
     o = torch.empty((1, 32, 128), device="cuda")

@@ -308,18 +308,21 @@ def test_error_codes(M):
         M.attn_decode_partial([sh], q, [0])   # G = 32
 
 
-def test_decode_step_host_single_gpu(M):
+@pytest.mark.parametrize("pinned", [True, False], ids=["zero-copy", "staged"])
+def test_decode_step_host_single_gpu(M, pinned):
     """The end-to-end C-ABI call (host buffers in, host buffers out) equals the device
-    path: append the new token, decode it, copy o/lse back."""
+    path: append the new token, decode it, copy o/lse back.  Pinned (mapped) host buffers
+    take the zero-copy path, pageable ones the cudaMemcpyAsync staging."""
     N, h_kv, G, d = 30000, 8, 4, 128
     k, v = make_global_kv(91, N, h_kv, d)
     q = synth.queries(91, 1, h_kv * G, d, amp=6.0)
     sh = to_shard(k, v, 0, N - 1, extra_cap=5)
     ws = M.decode_step_workspace(1, h_kv * G, h_kv, d)
-    o_h = torch.empty((h_kv * G, d), dtype=torch.float32).pin_memory()
-    l_h = torch.empty((h_kv * G,), dtype=torch.float32).pin_memory()
-    M.decode_step_host(None, sh, True, q[0].contiguous().pin_memory(), k[N - 1].contiguous().pin_memory(),
-                       v[N - 1].contiguous().pin_memory(), N - 1, o_h, l_h, ws)
+    host = (lambda t: t.pin_memory()) if pinned else (lambda t: t)
+    o_h = host(torch.empty((h_kv * G, d), dtype=torch.float32))
+    l_h = host(torch.empty((h_kv * G,), dtype=torch.float32))
+    M.decode_step_host(None, sh, True, host(q[0].contiguous()), host(k[N - 1].contiguous()),
+                       host(v[N - 1].contiguous()), N - 1, o_h, l_h, ws)
     torch.cuda.synchronize()
     assert sh.len == N
     o, l = M.attn_decode_partial([sh], q.cuda(), [N - 1])
