@@ -202,6 +202,25 @@ def test_prefill_vs_oracle(M, prefix, c, h_kv, G, d, amp):
         compare(o, lse, om, lm, what=f"prefill P0={prefix} c={c} G={G} d={d}")
 
 
+@pytest.mark.parametrize("d", [64, 128])
+def test_prefill_growing_max_rescales(M, d):
+    """Keys whose scale grows along the sequence make every few KV tiles raise the running
+    max past the lazy-rescale threshold (2^8), so O is rescaled in TMEM before the next P
+    chunk is handed to the MMA warp, tile after tile; the result must still match the oracle."""
+    prefix, c, h_kv, G = 6000, 200, 2, 4
+    N = prefix + c
+    k, v = make_global_kv(77, N, h_kv, d)
+    grow = (0.25 + torch.arange(N, dtype=torch.float32) / 1650.0)[:, None, None]   # logits std 0.5 -> 8
+    k = (k.float() * grow).to(torch.bfloat16)
+    q = synth.queries(77, c, h_kv * G, d, amp=2.0)
+    sh = to_shard(k, v, 0, N)
+    o, lse = M.attn_prefill_chunk(sh, q.cuda(), prefix)
+    om, lm = oracle_attention(q, k, v, list(range(prefix, N)))
+    # the row maxima climb by tens of log2 units over the KV range: several rescales per row
+    assert float(lm.max() - lm.min()) > 10.0
+    compare(o, lse, om, lm, what=f"prefill growing max d={d}")
+
+
 def test_prefill_chunked_equals_one_shot(M):
     """I2 on the GPU: chunks of any size over the growing KV equal one-shot causal prefill."""
     n, h_kv, G, d = 700, 2, 4, 128
