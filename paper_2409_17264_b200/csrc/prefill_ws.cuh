@@ -47,6 +47,13 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef MEDHA_PF_SETMAXNREG
 #define MEDHA_PF_SETMAXNREG 0   // rebalance registers between warpgroups (A/B knob)
 #endif
+#ifndef MEDHA_PF_NREG_LO
+#define MEDHA_PF_NREG_LO 80    // producer / MMA / allocator warpgroup
+#endif
+#ifndef MEDHA_PF_NREG_HI
+#define MEDHA_PF_NREG_HI 208   // softmax warpgroups
+#endif
+static_assert(128 * MEDHA_PF_NREG_LO + 256 * MEDHA_PF_NREG_HI <= 168 * 384, "register file");
 #ifndef MEDHA_PF_SPLIT_FMA
 #define MEDHA_PF_SPLIT_FMA 1   // x = (s*scale) - m in two roundings (partition-invariant P)
 #endif
@@ -303,17 +310,16 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-#if MEDHA_PF_SETMAXNREG
-  // rebalance the register file: producer/MMA warpgroup shrinks, softmax warpgroups grow
-  if (warp < 4)
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
-  else
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
-#endif
 
   uint8_t *sQ = smem + L::kQ0;
   auto slot_ptr = [&](int s) { return smem + L::kSlot0 + s * L::kSlotBytes; };
 
+  if (warp < 4) {
+#if MEDHA_PF_SETMAXNREG
+  // register file rebalance (all four warps of a warpgroup execute the same instruction, inside
+  // the branch so ptxas knows each region's budget): 128 x LO + 256 x HI <= 168 x 384
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(MEDHA_PF_NREG_LO) : "memory");
+#endif
   if (warp == 0) {
     // ================================ TMA producer ================================
     if (lane == 0 && n > 0) {
@@ -399,7 +405,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+#if MEDHA_PF_SETMAXNREG
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(MEDHA_PF_NREG_HI) : "memory");
+#endif
     // ================================ softmax + epilogue ==========================
     const int x = (warp - 4) >> 2;          // 0: tile A, 1: tile B
     const int r = tid - 128 - x * 128;      // row in tile = TMEM lane
