@@ -285,6 +285,54 @@ def bench_decode(args, rank, world, M):
                 o=o_out, sh=sh)
 
 
+def bench_graph_decode(M, iters=50, warm=5):
+    """configs[1] decode step replayed from ONE captured CUDA graph (device-side
+    lengths, `medha_decode_step_dev`): graph = reset the device length to 2^20 - 1, append the
+    token at it, decode over 2^20 keys (the device length then advances); same work per step
+    as the eager line."""
+    import torch
+    import synth
+    sh = build_shard(M, 0, 1, N_KV, H_KV, D)
+    new_pos = N_KV - 1
+    k_new = synth.kv_block(SEED, synth.STREAM_K, new_pos, 1, H_KV, D, device="cuda")
+    v_new = synth.kv_block(SEED, synth.STREAM_V, new_pos, 1, H_KV, D, device="cuda")
+    q = synth.queries(SEED, 1, H_Q, D, device="cuda", amp=4.0)
+    len0 = torch.tensor([new_pos], dtype=torch.int64, device="cuda")
+    len_dev = len0.clone()
+    ws = M.decode_workspace(1, H_Q, H_KV, D)
+    o = torch.empty((1, H_Q, D), dtype=torch.float32, device="cuda")
+    lse = torch.empty((1, H_Q), dtype=torch.float32, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            len_dev.copy_(len0)
+            M.decode_step_dev([sh], k_new, v_new, q, len_dev, o, lse, ws)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    o_eager = o.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        len_dev.copy_(len0)
+        M.decode_step_dev([sh], k_new, v_new, q, len_dev, o, lse, ws)
+    for _ in range(warm):
+        g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / iters
+    same = bool(torch.equal(o, o_eager))
+    del sh
+    torch.cuda.empty_cache()
+    return {"ms_per_step": round(ms, 5), "GBps": round(N_KV * H_KV * D * 2 * 2 / (ms * 1e-3) / 1e9, 1),
+            "graph": "length reset (memcpy) + kv_append_dev + decode, replayed", "replays": iters,
+            "output_equals_eager_call": same}
+
+
 def bench_prefill(M, sh_full, prefixes, chunks, iters=5, warm=2):
     """Chunked-prefill partial on one GPU at prefix P0 (configs[2]): the chunk's own
     K/V are rows [P0, P0+c) of the same synthetic sequence (already resident)."""
@@ -557,6 +605,7 @@ def main():
         del sh_p
         torch.cuda.empty_cache()
         extra["decode_70b_10M"] = bench_70b_decode(M)
+        extra["decode_cuda_graph"] = bench_graph_decode(M)
     if world in (1, 4) and not args.no_extra:
         mixed = bench_mixed(M, rank, world)
         if rank == 0:

@@ -263,6 +263,27 @@ medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, in
                                     void *ws, size_t ws_bytes, void *stream);
 
 /*
+ * decode_step_dev (device-side lengths, CUDA-graph-capturable; P:178-183
+ * decode scans the whole KV, P:597-599 per-shard partial).  One decode token for each of
+ * `batch` (1..64) sequences on this GPU, all lengths on the DEVICE:
+ *   1. k_new / v_new (bf16 [batch][h_kv][d], device) row b is appended to shard b at local
+ *      index len_dev[b] (int64 [batch], device; appends at or past the capacity are dropped);
+ *   2. sequence b attends keys 0..len_dev[b] of its shard (its own new token included; the
+ *      query is q[b], bf16 [batch][h_q][d], at position pos0 + len_dev[b]) -> o fp32
+ *      [batch][h_q][d], lse fp32 [batch][h_q] (natural log);
+ *   3. len_dev[b] += 1.
+ * Nothing on the host depends on the lengths: the split plan is fixed from kvs_host[b].capacity
+ * (splits past the current length are empty), so the same call - or a CUDA graph captured
+ * from it - can be replayed step after step.  kvs_host[b].len is neither read nor updated.
+ * Workspace: medha_decode_workspace_size(batch, h_q, h_kv, d), zeroed once.  Errors as
+ * medha_attn_decode_partial; ENOTSUP for batch > 64.
+ */
+medha_status medha_decode_step_dev(const medha_kv_shard *kvs_host, int32_t batch, const void *k_new,
+                                   const void *v_new, const void *q, int32_t h_q, int64_t *len_dev,
+                                   float scale, float *o, float *lse, void *ws, size_t ws_bytes,
+                                   void *stream);
+
+/*
  * hbm_read_probe (measurement aid K6): streams `bytes` bytes from
  * `src` with 16-byte loads and writes one word per CTA to `sink` (>= 4096 floats)
  * so the reads cannot be elided.  Gives the same-run read-only HBM bandwidth.

@@ -74,6 +74,7 @@ _sig("medha_kvp_prefill_chunk", _i32, _vp, _P(_Shard), _vp, _i64, _i32, _i64, _f
 _sig("medha_decode_step_workspace_size", _sz, _i32, _i32, _i32, _i32)
 _sig("medha_decode_step_host", _i32, _vp, _P(_Shard), _i32, _vp, _vp, _vp, _i32, _i64, _f32, _vp, _vp, _vp, _sz,
      _vp)
+_sig("medha_decode_step_dev", _i32, _P(_Shard), _i32, _vp, _vp, _vp, _i32, _vp, _f32, _vp, _vp, _vp, _sz, _vp)
 _sig("medha_hbm_read_probe", _i32, _vp, _sz, _vp, _vp)
 
 
@@ -391,6 +392,22 @@ def decode_step_host(comm: Optional[KVPComm], shard: KVShard, append: bool, q_ho
 
 def decode_step_workspace(world, h_q, h_kv, d, device=None):
     return _workspace(f"step{world}", lib.medha_decode_step_workspace_size(world, h_q, h_kv, d), device or "cuda")
+
+
+def decode_step_dev(shards: Sequence[KVShard], k_new: torch.Tensor, v_new: torch.Tensor, q: torch.Tensor,
+                    len_dev: torch.Tensor, o: torch.Tensor, lse: torch.Tensor, ws: torch.Tensor, scale=None,
+                    stream=None) -> None:
+    """Graph-capturable decode step with device-side lengths (include/medha_attn.h): append
+    k_new/v_new [B][h_kv][d] at len_dev[b], attend keys 0..len_dev[b], then len_dev += 1.
+    Host shard lengths are neither read nor updated."""
+    _need_cuda(k_new, "k_new", torch.bfloat16)
+    _need_cuda(v_new, "v_new", torch.bfloat16)
+    _need_cuda(q, "q", torch.bfloat16)
+    _need_cuda(len_dev, "len_dev", torch.int64)
+    B, h_q, d = q.shape
+    arr = _shards_c(shards)
+    _check(lib.medha_decode_step_dev(arr, B, _ptr(k_new), _ptr(v_new), _ptr(q), h_q, _ptr(len_dev), _scale(scale, d),
+                                     _ptr(o), _ptr(lse), _ptr(ws), ws.numel(), _stream(stream)), "decode_step_dev")
 
 
 def hbm_read_probe(src: torch.Tensor, sink: torch.Tensor, stream=None) -> None:

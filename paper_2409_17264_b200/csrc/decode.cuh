@@ -80,7 +80,9 @@ struct DecodeSeq {
   int64_t hstride;        // tokens between head planes (capacity, or pool_tokens when paged)
   const int32_t *pt;      // page table (paged KV) or null
   int32_t psl;            // log2(page size)
-  int64_t n_vis;         // visible local tokens (keys 0..n_vis-1)
+  int64_t n_vis;         // visible local tokens (keys 0..n_vis-1); with len_dev: an upper bound
+  int64_t *len_dev;       // device-length mode (graph-capturable step): keys 0..*len_dev are
+                          // visible (the token appended at *len_dev included), *len_dev += 1 at the end
   int32_t split_tokens;  // tokens per split, multiple of 64
   int32_t n_splits;      // splits per kv head
   int32_t cta_begin;     // first CTA of this sequence (CTAs ordered [kvh][split])
@@ -164,7 +166,10 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   const int kvh = local / S.n_splits;
   const int split = local - kvh * S.n_splits;
   const int64_t t_begin = (int64_t)split * S.split_tokens;
-  const int64_t t_end = min64(t_begin + S.split_tokens, S.n_vis);
+  // device-length mode: the visible length is read at run time (splits past it are empty:
+  // o = 0, lse = -inf, which the split merge ignores)
+  const int64_t n_vis = S.len_dev ? min64(S.n_vis, *S.len_dev + 1) : S.n_vis;
+  const int64_t t_end = min64(t_begin + S.split_tokens, n_vis);
 
   const __nv_bfloat16 *kbase = S.k + (int64_t)kvh * S.hstride * D;
   const __nv_bfloat16 *vbase = S.v + (int64_t)kvh * S.hstride * D;
@@ -592,6 +597,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     if (atomicAdd(p.work + 1, 1u) == gridDim.x - 1) {
       p.work[0] = 0u;
       p.work[1] = 0u;
+      // device-length mode: every item has read the lengths; advance them for the next step
+      for (int i = 0; i < p.n_seq; ++i)
+        if (p.seq[i].len_dev) *p.seq[i].len_dev += 1;
 #ifdef MEDHA_DECODE_TRACE
       g_ltrace[g_ltrace_n & 63][2] = gtimer();
       g_ltrace_n = g_ltrace_n + 1;

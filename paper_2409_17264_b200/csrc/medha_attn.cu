@@ -201,12 +201,15 @@ struct DecodeXchg {
   __nv_bfloat16 *obf;
 };
 
+// len_dev (device-length mode, medha_decode_step_dev): q_pos unused; sequence b attends keys
+// 0..len_dev[b] read at run time, the plan covers the shard's capacity, len_dev[b] += 1 after.
 medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const void *q, int32_t h_q,
                                  const int64_t *q_pos, float scale, float *o, float *lse, void *ws,
-                                 size_t ws_bytes, cudaStream_t st, const DecodeXchg *x = nullptr) {
+                                 size_t ws_bytes, cudaStream_t st, const DecodeXchg *x = nullptr,
+                                 int64_t *len_dev = nullptr) {
   if (batch < 0) return fail(MEDHA_EINVAL, "negative batch");
   if (batch == 0) return MEDHA_OK;
-  if (!kvs || !q || !q_pos || !o || !lse) return fail(MEDHA_EINVAL, "null argument");
+  if (!kvs || !q || !(q_pos || len_dev) || !o || !lse) return fail(MEDHA_EINVAL, "null argument");
   if (batch > 4096) return fail(MEDHA_ENOTSUP, "batch %d > 4096", batch);
   if (!aligned16(q)) return fail(MEDHA_EINVAL, "q not 16-byte aligned");
   if (!(scale > 0.f)) return fail(MEDHA_EINVAL, "scale must be > 0");
@@ -265,7 +268,8 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
     std::vector<int64_t> nvis(nb);
     for (int i = 0; i < nb; ++i) {
       const medha_kv_shard &kv = kvs[b0 + i];
-      nvis[i] = std::max<int64_t>(0, std::min<int64_t>(kv.len, q_pos[b0 + i] - kv.pos0 + 1));
+      nvis[i] = len_dev ? kv.capacity
+                        : std::max<int64_t>(0, std::min<int64_t>(kv.len, q_pos[b0 + i] - kv.pos0 + 1));
       total += nvis[i] * h_kv;
     }
     const int64_t per_cta =
@@ -285,6 +289,7 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
       S.pt = kv.page_table;
       S.psl = kv.page_table ? log2_pow2(kv.page_size) : 0;
       S.n_vis = nvis[i];
+      S.len_dev = len_dev ? len_dev + b0 + i : nullptr;
       S.split_tokens = (int32_t)split_tokens;
       S.n_splits = (int32_t)ns;
       S.cta_begin = cta;
@@ -1015,6 +1020,41 @@ medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, in
     if (lse_host) CUDA_TRY(cudaMemcpyAsync(lse_host, lse_dev, (size_t)h_q * 4, cudaMemcpyDeviceToHost, st));
   }
   return MEDHA_OK;
+}
+
+medha_status medha_decode_step_dev(const medha_kv_shard *kvs_host, int32_t batch, const void *k_new,
+                                   const void *v_new, const void *q, int32_t h_q, int64_t *len_dev, float scale,
+                                   float *o, float *lse, void *ws, size_t ws_bytes, void *stream) {
+  if (batch <= 0 || batch > kDecodeMaxSeqPerLaunch) return fail(MEDHA_ENOTSUP, "batch %d not in [1, 64]", batch);
+  if (!kvs_host || !k_new || !v_new || !q || !len_dev || !o || !lse) return fail(MEDHA_EINVAL, "null argument");
+  if (!aligned16(k_new) || !aligned16(v_new) || (reinterpret_cast<uintptr_t>(len_dev) & 7))
+    return fail(MEDHA_EINVAL, "k_new/v_new not 16-byte aligned or len_dev not 8-byte aligned");
+  const int32_t h_kv = kvs_host[0].h_kv, d = kvs_host[0].d;
+  AppendDevParams ap;
+  memset(&ap, 0, sizeof(ap));
+  for (int b = 0; b < batch; ++b) {
+    const medha_kv_shard &kv = kvs_host[b];
+    medha_status s = check_shard(&kv);
+    if (s) return s;
+    if (kv.h_kv != h_kv || kv.d != d) return fail(MEDHA_ESHAPE, "shards disagree on h_kv/d");
+    ap.seq[b].k = static_cast<uint4 *>(kv.k);
+    ap.seq[b].v = static_cast<uint4 *>(kv.v);
+    ap.seq[b].hstride = head_stride(kv);
+    ap.seq[b].cap = kv.capacity;
+    ap.seq[b].pt = kv.page_table;
+    ap.seq[b].psl = kv.page_table ? log2_pow2(kv.page_size) : 0;
+  }
+  ap.k_new = static_cast<const uint4 *>(k_new);
+  ap.v_new = static_cast<const uint4 *>(v_new);
+  ap.len_dev = len_dev;
+  ap.batch = batch;
+  ap.h_kv = h_kv;
+  ap.vec_per_row = d / 8;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t total = (int64_t)batch * h_kv * (d / 8);
+  launch_pdl(kv_append_dev_kernel, dim3((unsigned)cdiv(total, 256)), dim3(256), 0, st, ap);
+  LAUNCH_CHECK("kv_append_dev_kernel");
+  return decode_partial_impl(kvs_host, batch, q, h_q, nullptr, scale, o, lse, ws, ws_bytes, st, nullptr, len_dev);
 }
 
 #ifdef MEDHA_DECODE_TRACE
