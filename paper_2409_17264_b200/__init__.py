@@ -96,8 +96,9 @@ def _ptr(t: Optional[torch.Tensor]):
 
 
 def _stream(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    if stream is None:   # raw handle of the current stream, without building a Stream object
+        return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch.cuda.current_device()))
+    return ctypes.c_void_p(stream.cuda_stream)
 
 
 def _need_cuda(t: torch.Tensor, name: str, dtype=None):

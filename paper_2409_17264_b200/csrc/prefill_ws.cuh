@@ -257,9 +257,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   constexpr int NH = D / 64;
   constexpr uint32_t kIdescS = umma_idesc_bf16(kWsTileM, kWsTileN, 0);
   constexpr uint32_t kIdescO = umma_idesc_bf16(kWsTileM, D, 1);
-  pdl_wait();                 // PDL: the previous kernel on the stream (e.g. kv_append) is done
-  pdl_launch_dependents();    // the split merge may take SMs as this grid's last wave retires
-
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kBar);
@@ -306,10 +303,20 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     mbar_fence_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(tmq);
+    tma_prefetch_desc(tmk);
+    tma_prefetch_desc(tmv);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the set-up above touches only this CTA's shared memory, TMEM and kernel parameters,
+  // so it overlaps the previous kernel's tail; global memory (Q, K/V written by e.g.
+  // kv_append, outputs read by e.g. the previous split merge) only after this wait
+  pdl_wait();
+  pdl_launch_dependents();    // the split merge may take SMs as this grid's last wave retires
 
   uint8_t *sQ = smem + L::kQ0;
   auto slot_ptr = [&](int s) { return smem + L::kSlot0 + s * L::kSlotBytes; };
@@ -323,9 +330,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   if (warp == 0) {
     // ================================ TMA producer ================================
     if (lane == 0 && n > 0) {
-      tma_prefetch_desc(tmq);
-      tma_prefetch_desc(tmk);
-      tma_prefetch_desc(tmv);
       mbar_arrive_expect_tx(bar_q, 2 * L::kQBytes);
 #pragma unroll
       for (int x = 0; x < 2; ++x)
