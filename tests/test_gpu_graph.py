@@ -122,3 +122,38 @@ def test_decode_step_dev_errors(M):
                           torch.zeros((65, 8, 128), dtype=torch.bfloat16, device="cuda"),
                           torch.zeros((65, 32, 128), dtype=torch.bfloat16, device="cuda"),
                           torch.zeros(65, dtype=torch.int64, device="cuda"), o, lse, ws)
+
+
+@pytest.mark.parametrize("ps,G,d", [(16, 8, 128), (128, 4, 64)])
+def test_decode_step_dev_paged(M, ps, G, d):
+    """Device-length steps on paged shards (random page order, NaN-poisoned pool): the append
+    goes through the page table at the device length, the decode sees exactly keys 0..len."""
+    import math
+    from test_gpu_paged import Pool, paged_shards
+    rng = np.random.default_rng(ps + G)
+    h_kv, steps = 2, 3
+    lens = [int(rng.integers(1, 3000)) for _ in range(3)]
+    need = [math.ceil((n + steps) / ps) for n in lens]
+    pool = Pool(sum(need) + 4, ps, h_kv, d, float("nan"), rng)
+    ks, vs, specs = [], [], []
+    for b, n in enumerate(lens):
+        k, v = make_global_kv(8100 + b, n + steps, h_kv, d)
+        pages = pool.take(need[b])
+        pool.fill(pages, k, v, 0, n)
+        ks.append(k)
+        vs.append(v)
+        specs.append((pages, n, 0))
+    shards = paged_shards(M, pool, specs)
+    B, h_q = len(lens), h_kv * G
+    len_dev = torch.tensor(lens, dtype=torch.int64, device="cuda")
+    ws = M.decode_workspace(B, h_q, h_kv, d)
+    o = torch.empty((B, h_q, d), device="cuda")
+    lse = torch.empty((B, h_q), device="cuda")
+    for t in range(steps):
+        k_new = torch.stack([ks[b][lens[b] + t] for b in range(B)]).cuda()
+        v_new = torch.stack([vs[b][lens[b] + t] for b in range(B)]).cuda()
+        q = synth.queries(8200 + t, B, h_q, d, amp=4.0)
+        M.decode_step_dev(shards, k_new, v_new, q.cuda(), len_dev, o, lse, ws)
+        torch.cuda.synchronize()
+        _check_step(M, ks, vs, lens, t, q, o, lse, f"paged decode_step_dev ps={ps}")
+    assert len_dev.tolist() == [n + steps for n in lens]
