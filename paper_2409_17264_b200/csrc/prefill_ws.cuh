@@ -18,7 +18,8 @@
 //   warp 2      TMEM allocator (512 columns: S_A | S_B | O_A | O_B).
 //   warps 4-7   softmax of tile A, warps 8-11 softmax of tile B: thread = TMEM lane =
 //               query row.  Two passes over S (row max, then exp2/sum/pack), P as bf16
-//               back into TMEM with tcgen05.st.  The running max is only raised when
+//               back into TMEM with tcgen05.st, handed to the MMA warp in two 64-key
+//               chunks (PV of keys 0-63 overlaps the exponentials of keys 64-127).  The running max is only raised when
 //               it grows by more than 2^8 (exact: numerator and denominator use the
 //               same stale max; p <= 256 stays finite in bf16/fp32), so O is rarely
 //               rescaled; when it is, the softmax warps rescale O_X in TMEM.
