@@ -1074,6 +1074,10 @@ medha_status medha_debug_pf_trace(long long *host_out /* [512][12] */) {
   CUDA_TRY(cudaMemcpyFromSymbol(host_out, g_pf_trace, sizeof(g_pf_trace)));
   return MEDHA_OK;
 }
+medha_status medha_debug_pf_gtimer(long long *host_out /* [8] */) {
+  CUDA_TRY(cudaMemcpyFromSymbol(host_out, g_pf_gt, sizeof(g_pf_gt)));
+  return MEDHA_OK;
+}
 #endif
 
 medha_status medha_hbm_read_probe(const void *src, size_t bytes, float *sink, void *stream) {

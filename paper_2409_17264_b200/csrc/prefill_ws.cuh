@@ -73,6 +73,14 @@ constexpr int kPChunks = 2;   // P handed to the MMA warp in two 64-key chunks
 #ifdef MEDHA_PF_TRACE
 // experiment only: clock64 stamps of the hand-offs in CTA 0, per KV tile (medha_debug_pf_trace)
 __device__ long long g_pf_trace[512][12];
+// %globaltimer (ns) of CTA 0: [0] entry, [1] past griddepcontrol.wait, [2] S_A(0) seen,
+// [3] last P of tile A stored, [4] tile A's outputs stored; [5] = clock64 at [2], [6] at [3]
+__device__ long long g_pf_gt[8];
+__device__ __forceinline__ long long pf_gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define PF_STAMP(j, k)                                                  \
   do {                                                                  \
     if (blockIdx.x == 0 && (j) < 512) g_pf_trace[(j)][(k)] = clock64(); \
@@ -258,6 +266,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   constexpr int NH = D / 64;
   constexpr uint32_t kIdescS = umma_idesc_bf16(kWsTileM, kWsTileN, 0);
   constexpr uint32_t kIdescO = umma_idesc_bf16(kWsTileM, D, 1);
+#ifdef MEDHA_PF_TRACE
+  const long long gt_entry = pf_gtimer();
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kBar);
@@ -318,6 +329,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   // kv_append, outputs read by e.g. the previous split merge) only after this wait
   pdl_wait();
   pdl_launch_dependents();    // the split merge may take SMs as this grid's last wave retires
+#ifdef MEDHA_PF_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g_pf_gt[0] = gt_entry;
+    g_pf_gt[1] = pf_gtimer();
+  }
+#endif
 
   uint8_t *sQ = smem + L::kQ0;
   auto slot_ptr = [&](int s) { return smem + L::kSlot0 + s * L::kSlotBytes; };
@@ -435,6 +452,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     for (int j = 0; j < n; ++j) {
       mbar_wait(bar_s + x, j & 1);
       if ((warp & 3) == 0 && lane == 0) PF_STAMP(j, 4 * x + 0);
+#ifdef MEDHA_PF_TRACE
+      if (blockIdx.x == 0 && warp == 4 && lane == 0 && j == 0) {
+        g_pf_gt[2] = pf_gtimer();
+        g_pf_gt[5] = clock64();
+      }
+#endif
       __syncwarp();
       tc_fence_after();
 #if MEDHA_PF_ABLATE == 1
@@ -496,6 +519,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       m_run = m_use;
       const float lsum = lsum2.x + lsum2.y;
       if ((warp & 3) == 0 && lane == 0) PF_STAMP(j, 4 * x + 3);
+#ifdef MEDHA_PF_TRACE
+      if (blockIdx.x == 0 && warp == 4 && lane == 0 && j == n - 1) {
+        g_pf_gt[3] = pf_gtimer();
+        g_pf_gt[6] = clock64();
+      }
+#endif
       l_run = l_run * alpha + lsum;
     }
 
@@ -538,6 +567,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       }
     }
     if (row_valid) *lrow = lse_nat;
+#ifdef MEDHA_PF_TRACE
+    if (blockIdx.x == 0 && warp == 4 && lane == 0) g_pf_gt[4] = pf_gtimer();
+#endif
   }
 
   tc_fence_before();

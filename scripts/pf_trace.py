@@ -8,7 +8,7 @@ import numpy as np
 import torch
 import bench, synth
 import paper_2409_17264_b200 as M
-for P0, c in ((131072, 1024), (131072, 64)):
+for P0, c in ((131072, 64), (131072, 1024)):
     sh = bench.build_range(M, 0, P0 + c, 8, 128)
     q = synth.queries(3, c, 32, 128, device="cuda")
     for _ in range(3):
@@ -34,5 +34,13 @@ for P0, c in ((131072, 1024), (131072, 64)):
         np.median(mid[:, 1] - mid[:, 0]), np.median(mid[:, 2] - mid[:, 1]), np.median(mid[:, 3] - mid[:, 2]),
         np.median(mid[:, 8] - mid[:, 3]), np.median(mid[:, 9] - mid[:, 7]), np.median(mid[:, 4] - mid[:, 0])))
     # S_A(j+1) seen minus P_A(j) seen by the MMA warp = PV_A(j) + S_A(j+1) on the tensor pipe (+ queueing behind B)
+    span = int(max(t[n - 1, 3], t[n - 1, 7]) - t[0, 0])
+    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a_ev.record()
+    M.attn_prefill_chunk(sh, q, P0)
+    b_ev.record()
+    torch.cuda.synchronize()
+    print("loop span of CTA 0 (S_A(0) seen -> last P stored): %d clk; one call (prefill + split merge) %.1f us" % (
+        span, a_ev.elapsed_time(b_ev) * 1e3))
     print("median S_A(j+1) seen - P_A(j) seen by MMA: %d ; S_B(j+1) seen - P_B(j) seen: %d" % (
         np.median(t[3:n - 1, 0] - t[2:n - 2, 8]), np.median(t[3:n - 1, 4] - t[2:n - 2, 9])))
