@@ -4,7 +4,7 @@
  * sequence dimension, on NVIDIA B200 (sm_100a).
  *
  * Citations: "P:n" = PAPER.md line n of the paper's LaTeX source, "S:n" = the
- * SPEC.md line n written from it (see DESIGN.md for the readings R1-R18 of the
+ * SPEC.md line n written from it (see DESIGN.md for the readings R1-R22 of the
  * places where the paper is silent).
  *
  * What the library computes (P:167-171 attention; P:597-599 KVP):
@@ -166,9 +166,10 @@ medha_status medha_attn_prefill_batch(const medha_prefill_chunk *chunks_host, in
  * holds o_r [rows][d] followed by lse_r [rows].  Writes o_out fp32 [rows][d],
  * lse_out fp32 [rows] (may be NULL) and o_out_bf16 bf16 [rows][d] (may be NULL).
  * Parts are combined in order r = 0..P-1.  1 <= P <= 64.
- * A row whose parts are all -inf yields o = 0, lse = -inf; the call then still
- * completes but returns nothing different (the condition is data-dependent and
- * only visible on the device).
+ * A row whose parts are all -inf yields o = 0, lse = -inf and the call returns
+ * MEDHA_OK (reading R22: the condition is data-dependent and only visible
+ * on the device, and the calls never synchronise, so it cannot be an error status;
+ * an all-empty row is the exact merge of empty shards, R7).
  */
 medha_status medha_merge_partials(const float *parts, int32_t P, int64_t rows, int32_t d,
                                   float *o_out, float *lse_out, void *o_out_bf16, void *stream);
@@ -188,17 +189,37 @@ medha_status medha_kvp_comm_destroy(medha_kvp_comm *comm);
 medha_status medha_kvp_comm_info(const medha_kvp_comm *comm, int32_t *rank, int32_t *world);
 /*
  * Fused peer-to-peer exchange (single node, NVLink).  medha_kvp_comm_create also
- * allocates a receive buffer (~2 x world x 2.1 MB + flags) and maps every peer's buffer
- * through CUDA IPC (a collective; skipped when MEDHA_KVP_P2P=0 or when any rank fails).
- * When active, medha_kvp_decode (batch <= 64) runs the exchange inside the decode kernel:
- * the last CTA of each (sequence, kv head) stores the rank partial into every rank's
- * receive slot over NVLink, raises the peers' epoch flags (release, system scope), waits
- * for all ranks' flags (acquire) and merges in rank order - no NCCL call, no merge launch.
+ * allocates a receive buffer (~2 x world x 2.1 MB + flags + an epoch word) and maps every
+ * peer's buffer through CUDA IPC (a collective; skipped when MEDHA_KVP_P2P=0 or when any rank
+ * fails; at world 1 the local buffer serves as its own peer).  When active, medha_kvp_decode
+ * (batch <= 64) runs the exchange inside the decode kernel: the last CTA of each (sequence,
+ * kv head) stores the rank partial into every rank's receive slot over NVLink, raises the
+ * peers' epoch flags (release, system scope), waits for all ranks' flags (acquire) and merges
+ * in rank order - no NCCL call, no merge launch.  The call's epoch is read from and advanced
+ * in device memory by the kernel itself, so medha_kvp_decode may be captured in a CUDA graph
+ * and replayed (every rank must replay it the same number of times).
  * medha_kvp_comm_p2p returns 1 when that path is active; medha_kvp_comm_set_p2p(comm, 0)
  * forces the NCCL all-gather + merge path (must be switched identically on all ranks).
  */
 int32_t medha_kvp_comm_p2p(const medha_kvp_comm *comm);
 medha_status medha_kvp_comm_set_p2p(medha_kvp_comm *comm, int32_t enable);
+
+/*
+ * Failure containment of the fused exchange.  The in-kernel wait for a peer's
+ * partial is bounded by a timeout (default 30 s, env MEDHA_KVP_TIMEOUT_MS, or
+ * medha_kvp_comm_set_timeout in nanoseconds).  On expiry - a rank that never launched its
+ * call, e.g. after failing its own argument checks, or ranks that disagree on batch / h_q -
+ * the kernel writes NaN into the affected outputs, sets an error word in mapped host memory
+ * and finishes instead of hanging the GPU.  The communicator is then BROKEN for good:
+ * medha_kvp_comm_status (non-blocking; meaningful once the stream has been synchronised) and
+ * every later collective call on it return MEDHA_ENCCL; destroy it and create a new one.
+ * medha_kvp_comm_debug(comm, 1) is a test hook: this rank's decode kernels withhold their
+ * pushes and flags (so every waiting rank, itself included, times out); 0 restores normal
+ * operation.
+ */
+medha_status medha_kvp_comm_status(medha_kvp_comm *comm);
+medha_status medha_kvp_comm_set_timeout(medha_kvp_comm *comm, uint64_t timeout_ns);
+medha_status medha_kvp_comm_debug(medha_kvp_comm *comm, uint32_t flags);
 
 /*
  * kvp_decode (Eq. 5): the local partial (medha_attn_decode_partial on

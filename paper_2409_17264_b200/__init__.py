@@ -65,6 +65,9 @@ _sig("medha_kvp_comm_destroy", _i32, _vp)
 _sig("medha_kvp_comm_info", _i32, _vp, _P(_i32), _P(_i32))
 _sig("medha_kvp_comm_p2p", _i32, _vp)
 _sig("medha_kvp_comm_set_p2p", _i32, _vp, _i32)
+_sig("medha_kvp_comm_status", _i32, _vp)
+_sig("medha_kvp_comm_set_timeout", _i32, _vp, ctypes.c_uint64)
+_sig("medha_kvp_comm_debug", _i32, _vp, ctypes.c_uint32)
 _sig("medha_kvp_workspace_size", _sz, _i32, _i32, _i32, _i32, _i32)
 _sig("medha_kvp_decode", _i32, _vp, _P(_Shard), _i32, _vp, _i32, _P(_i64), _f32, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("medha_kvp_exchange_workspace_size", _sz, _i32, _i64, _i32)
@@ -165,9 +168,14 @@ def _scale(scale, d):
 _WS = {}
 
 
-def _workspace(kind: str, nbytes: int, device) -> torch.Tensor:
-    """Cached zero-initialised workspace (the library leaves counters zeroed)."""
-    key = (kind, torch.device(device).index)
+def _workspace(kind: str, nbytes: int, device, stream=None) -> torch.Tensor:
+    """Cached zero-initialised workspace (the library leaves counters zeroed), one per
+    (kind, device, stream): calls that may run concurrently on different streams must not
+    share a workspace (include/medha_attn.h)."""
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    sid = stream.cuda_stream if stream is not None else torch._C._cuda_getCurrentRawStream(idx)
+    key = (kind, idx, sid)
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
@@ -175,16 +183,16 @@ def _workspace(kind: str, nbytes: int, device) -> torch.Tensor:
     return ws
 
 
-def decode_workspace(batch, h_q, h_kv, d, device=None):
-    return _workspace("decode", lib.medha_decode_workspace_size(batch, h_q, h_kv, d), device or "cuda")
+def decode_workspace(batch, h_q, h_kv, d, device=None, stream=None):
+    return _workspace("decode", lib.medha_decode_workspace_size(batch, h_q, h_kv, d), device or "cuda", stream)
 
 
-def prefill_workspace(c, h_q, h_kv, d, device=None):
-    return _workspace("prefill", lib.medha_prefill_workspace_size(c, h_q, h_kv, d), device or "cuda")
+def prefill_workspace(c, h_q, h_kv, d, device=None, stream=None):
+    return _workspace("prefill", lib.medha_prefill_workspace_size(c, h_q, h_kv, d), device or "cuda", stream)
 
 
-def kvp_workspace(world, batch, h_q, h_kv, d, device=None):
-    return _workspace("kvp", lib.medha_kvp_workspace_size(world, batch, h_q, h_kv, d), device or "cuda")
+def kvp_workspace(world, batch, h_q, h_kv, d, device=None, stream=None):
+    return _workspace("kvp", lib.medha_kvp_workspace_size(world, batch, h_q, h_kv, d), device or "cuda", stream)
 
 
 def kv_append(shard: KVShard, k_new: torch.Tensor, v_new: torch.Tensor, stream=None) -> None:
@@ -211,7 +219,7 @@ def attn_decode_partial(shards: Sequence[KVShard], q: torch.Tensor, q_pos: Seque
         lse = torch.empty((B, h_q), dtype=torch.float32, device=q.device)
     h_kv = shards[0].h_kv
     if ws is None:
-        ws = decode_workspace(B, h_q, h_kv, d, q.device)
+        ws = decode_workspace(B, h_q, h_kv, d, q.device, stream)
     qp = (ctypes.c_int64 * B)(*[int(x) for x in q_pos])
     _check(lib.medha_attn_decode_partial(_shards_c(shards), B, _ptr(q), h_q, qp, _scale(scale, d), _ptr(o),
                                          _ptr(lse), _ptr(ws), ws.numel(), _stream(stream)), "attn_decode_partial")
@@ -228,7 +236,7 @@ def attn_prefill_chunk(shard: KVShard, q: torch.Tensor, q_pos0: int, scale=None,
     if lse is None:
         lse = torch.empty((c, h_q), dtype=torch.float32, device=q.device)
     if ws is None:
-        ws = prefill_workspace(c, h_q, shard.h_kv, d, q.device)
+        ws = prefill_workspace(c, h_q, shard.h_kv, d, q.device, stream)
     sh = shard.c()
     _check(lib.medha_attn_prefill_chunk(ctypes.byref(sh), _ptr(q), c, h_q, int(q_pos0), _scale(scale, d), _ptr(o),
                                         _ptr(lse), _ptr(ws), ws.numel(), _stream(stream)), "attn_prefill_chunk")
@@ -266,7 +274,8 @@ def attn_prefill_batch(shards: Sequence[KVShard], qs: Sequence[torch.Tensor], q_
         outs.append((o, lse))
     if ws is None:
         cs_arr = (ctypes.c_int64 * n)(*[q.shape[0] for q in qs])
-        ws = _workspace("prefill_batch", lib.medha_prefill_batch_workspace_size(n, cs_arr, h_q, d), qs[0].device)
+        ws = _workspace("prefill_batch", lib.medha_prefill_batch_workspace_size(n, cs_arr, h_q, d), qs[0].device,
+                        stream)
     _check(lib.medha_attn_prefill_batch(arr, n, h_q, _scale(scale, d), _ptr(ws), ws.numel(), _stream(stream)),
            "attn_prefill_batch")
     return outs
@@ -292,15 +301,38 @@ class KVPComm:
     communicator on its current CUDA device.
     """
 
-    def __init__(self, group=None):
-        import torch.distributed as dist
-        from .kvp import exchange_unique_id
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
-        uid = (ctypes.c_uint8 * 128).from_buffer_copy(exchange_unique_id(group))
+    def __init__(self, group=None, _single=False):
+        if _single:       # a one-rank group, no process group needed (KVPComm.single())
+            self.rank, self.world = 0, 1
+            uid = (ctypes.c_uint8 * 128)()
+            _check(lib.medha_kvp_unique_id(uid), "kvp_unique_id")
+        else:
+            import torch.distributed as dist
+            from .kvp import exchange_unique_id
+            self.rank = dist.get_rank(group)
+            self.world = dist.get_world_size(group)
+            uid = (ctypes.c_uint8 * 128).from_buffer_copy(exchange_unique_id(group))
         h = ctypes.c_void_p()
         _check(lib.medha_kvp_comm_create(uid, self.rank, self.world, ctypes.byref(h)), "kvp_comm_create")
         self.handle = h
+
+    @classmethod
+    def single(cls) -> "KVPComm":
+        """A KVP group of one rank on the current device (world 1): the full KVP path
+        (fused self-exchange or NCCL all-gather of one part, then the merge) on one GPU."""
+        return cls(_single=True)
+
+    def status(self) -> int:
+        """medha_kvp_comm_status: 0, or MEDHA_ENCCL (-7) once a fused-exchange wait timed out."""
+        return int(lib.medha_kvp_comm_status(self.handle))
+
+    def set_timeout(self, seconds: float) -> None:
+        """Bound of the in-kernel wait for peers' partials (default 30 s)."""
+        _check(lib.medha_kvp_comm_set_timeout(self.handle, int(seconds * 1e9)), "kvp_comm_set_timeout")
+
+    def debug(self, flags: int) -> None:
+        """Test hook (medha_kvp_comm_debug): 1 = this rank withholds its exchange pushes."""
+        _check(lib.medha_kvp_comm_debug(self.handle, int(flags)), "kvp_comm_debug")
 
     @property
     def p2p(self) -> bool:
@@ -337,15 +369,15 @@ def kvp_decode(comm: KVPComm, shards: Sequence[KVShard], q: torch.Tensor, q_pos:
         lse = torch.empty((B, h_q), dtype=torch.float32, device=q.device)
     ob = torch.empty((B, h_q, d), dtype=torch.bfloat16, device=q.device) if want_bf16 else None
     if ws is None:
-        ws = kvp_workspace(comm.world, B, h_q, shards[0].h_kv, d, q.device)
+        ws = kvp_workspace(comm.world, B, h_q, shards[0].h_kv, d, q.device, stream)
     qp = (ctypes.c_int64 * B)(*[int(x) for x in q_pos])
     _check(lib.medha_kvp_decode(comm.handle, _shards_c(shards), B, _ptr(q), h_q, qp, _scale(scale, d), _ptr(o),
                                 _ptr(lse), _ptr(ob), _ptr(ws), ws.numel(), _stream(stream)), "kvp_decode")
     return o, lse, ob
 
 
-def exchange_workspace(world, rows, d, device=None):
-    return _workspace(f"xchg{world}", lib.medha_kvp_exchange_workspace_size(world, rows, d), device or "cuda")
+def exchange_workspace(world, rows, d, device=None, stream=None):
+    return _workspace(f"xchg{world}", lib.medha_kvp_exchange_workspace_size(world, rows, d), device or "cuda", stream)
 
 
 def kvp_exchange_merge(comm: KVPComm, send: torch.Tensor, rows: int, d: int, o_out: torch.Tensor,
@@ -354,7 +386,7 @@ def kvp_exchange_merge(comm: KVPComm, send: torch.Tensor, rows: int, d: int, o_o
     """a6 + a7: all-gather this rank's packed (o, lse) partial and merge in rank order."""
     _need_cuda(send, "send", torch.float32)
     if ws is None:
-        ws = exchange_workspace(comm.world, rows, d, send.device)
+        ws = exchange_workspace(comm.world, rows, d, send.device, stream)
     _check(lib.medha_kvp_exchange_merge(comm.handle, _ptr(send), rows, d, _ptr(o_out), _ptr(lse_out), _ptr(o_bf16),
                                         _ptr(ws), ws.numel(), _stream(stream)), "kvp_exchange_merge")
 
@@ -369,7 +401,7 @@ def kvp_prefill_chunk(comm: KVPComm, shard: KVShard, q: torch.Tensor, q_pos0: in
     ob = torch.empty((c, h_q, d), dtype=torch.bfloat16, device=q.device) if want_bf16 else None
     if ws is None:
         ws = _workspace("kvp_prefill", lib.medha_kvp_prefill_workspace_size(comm.world, c, h_q, shard.h_kv, d),
-                        q.device)
+                        q.device, stream)
     sh = shard.c()
     _check(lib.medha_kvp_prefill_chunk(comm.handle, ctypes.byref(sh), _ptr(q), c, h_q, int(q_pos0), _scale(scale, d),
                                        _ptr(o), _ptr(lse), _ptr(ob), _ptr(ws), ws.numel(), _stream(stream)),
@@ -391,8 +423,9 @@ def decode_step_host(comm: Optional[KVPComm], shard: KVShard, append: bool, q_ho
     shard.len = sh.len
 
 
-def decode_step_workspace(world, h_q, h_kv, d, device=None):
-    return _workspace(f"step{world}", lib.medha_decode_step_workspace_size(world, h_q, h_kv, d), device or "cuda")
+def decode_step_workspace(world, h_q, h_kv, d, device=None, stream=None):
+    return _workspace(f"step{world}", lib.medha_decode_step_workspace_size(world, h_q, h_kv, d), device or "cuda",
+                      stream)
 
 
 def decode_step_dev(shards: Sequence[KVShard], k_new: torch.Tensor, v_new: torch.Tensor, q: torch.Tensor,

@@ -104,19 +104,23 @@ struct DecodeParams {
   int32_t h_q;
   // ---- fused KVP exchange over NVLink.  x_world == 0: off. ----
   // The last CTA of every (seq, kv head) pushes the unit's rank partial into every rank's
-  // receive slot (peer memory mapped with CUDA IPC), raises that rank's flag for the unit
-  // to `x_epoch` (release, system scope), waits for the flags of all ranks (acquire) and
-  // merges the world's partials in rank order into x_o / x_lse / x_obf.
+  // receive slot (peer memory mapped with CUDA IPC; at world 1 the local buffer), raises
+  // that rank's flag for the unit to the call's epoch (release, system scope), waits for
+  // the flags of all ranks (acquire, bounded by x_timeout_ns) and merges the world's
+  // partials in rank order into x_o / x_lse / x_obf.  The epoch lives in DEVICE memory
+  // (*x_epoch = last completed call, advanced by the last CTA out), so a captured CUDA
+  // graph replays with a fresh epoch every time.  Buffer layout of every rank (XchgLayout):
+  // [2 parities][world src][x_slot floats] slots, [2][world][x_units] flags, epoch word.
   int32_t x_world;
   int32_t x_rank;
-  uint32_t x_epoch;
   int32_t x_units;                 // flag stride per source rank
+  uint32_t x_debug;                // test hook: bit 0 = withhold this rank's pushes and flags
   int64_t x_rows;                  // rows of the packed slot layout: o [x_rows][D], lse [x_rows]
   int64_t x_slot;                  // floats per source-rank slot
-  float *x_dst[kMaxKvpRanks];      // rank r's receive slot for THIS rank (parity resolved)
-  uint32_t *x_flag_dst[kMaxKvpRanks];  // rank r's flags for THIS rank: [x_units]
-  const float *x_recv;             // local receive slots: [x_world][x_slot]
-  const uint32_t *x_flags;         // local flags: [x_world][x_units]
+  uint64_t x_timeout_ns;           // bound of the flag wait (%globaltimer)
+  char *x_peer[kMaxKvpRanks];      // every rank's exchange buffer (x_peer[x_rank] = local)
+  uint32_t *x_epoch;               // local device word: epoch of the last completed call
+  uint32_t *x_err;                 // mapped host word: set to 1 when a flag wait times out
   float *x_o;                      // final outputs [rows][D]
   float *x_lse;                    // final lse [rows] (may be null)
   __nv_bfloat16 *x_obf;            // final bf16 outputs (may be null)
@@ -132,6 +136,20 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *ptr) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// exchange buffer of one rank: receive slot / flags of (parity, source rank)
+__device__ __forceinline__ float *xchg_slot(const DecodeParams &p, char *base, uint32_t par, int src) {
+  return reinterpret_cast<float *>(base) + ((int64_t)par * p.x_world + src) * p.x_slot;
+}
+__device__ __forceinline__ uint32_t *xchg_flags(const DecodeParams &p, char *base, uint32_t par, int src) {
+  return reinterpret_cast<uint32_t *>(base + (size_t)2 * p.x_world * p.x_slot * sizeof(float)) +
+         ((int64_t)par * p.x_world + src) * p.x_units;
+}
+
 template <int D, int G>
 struct __align__(16) DecodeSmem {
   float o[kDecodeWarps][G][D];   // warp partials; later the warp sums of the split merge
@@ -140,6 +158,7 @@ struct __align__(16) DecodeSmem {
   float w[kDecodeSplitW];        // split (or rank) merge weights [split][G]
   unsigned ticket;
   int item;
+  uint32_t epoch;                // fused exchange: this call's epoch (kept out of registers)
 };
 
 // One work item: split `split` of kv head `kvh` of sequence `sidx`.
@@ -442,7 +461,9 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
       const float lse_r = (L > 0.f) ? (M + __log2f(L)) * kLn2 : -INFINITY;
       const int64_t orow = (int64_t)sidx * p.h_q + (int64_t)kvh * G + row;
       if (p.x_world > 0) {
-        for (int r = 0; r < p.x_world; ++r) p.x_dst[r][p.x_rows * D + orow] = lse_r;   // NVLink stores
+        if (!(p.x_debug & 1u))
+          for (int r = 0; r < p.x_world; ++r)
+            xchg_slot(p, p.x_peer[r], sm.epoch & 1u, p.x_rank)[p.x_rows * D + orow] = lse_r;   // NVLink stores
       } else {
         p.lse[orow] = lse_r;
       }
@@ -496,7 +517,8 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
     constexpr int WS = G * D;   // one warp's [G][D] block
     const float o = ((w0[idx] + w0[WS + idx]) + w0[2 * WS + idx]) + w0[3 * WS + idx];   // fixed order
     if (p.x_world > 0) {
-      for (int r = 0; r < p.x_world; ++r) p.x_dst[r][obase + idx] = o;                   // NVLink stores
+      if (!(p.x_debug & 1u))
+        for (int r = 0; r < p.x_world; ++r) xchg_slot(p, p.x_peer[r], sm.epoch & 1u, p.x_rank)[obase + idx] = o;
     } else {
       p.o[obase + idx] = o;
     }
@@ -509,45 +531,72 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
     if (tid == 0) __threadfence_system();
     __syncthreads();
     const int unit = sidx * p.h_kv + kvh;
-    if (tid < p.x_world) st_release_sys(p.x_flag_dst[tid] + unit, p.x_epoch);
+    if (tid < p.x_world && !(p.x_debug & 1u))
+      st_release_sys(xchg_flags(p, p.x_peer[tid], sm.epoch & 1u, p.x_rank) + unit, sm.epoch);
   }
   MEDHA_TRACE(3);
 }
 
 // Fused exchange, second half: wait until every rank's partial of `unit` has arrived
-// (acquire) and merge them in rank order (same formula as lse_merge_kernel).
+// (acquire) and merge them in rank order (same formula as lse_merge_kernel).  The wait is
+// bounded: after x_timeout_ns without a peer's flag (a rank that never launched, or a
+// collective-contract violation) the unit's outputs become NaN, *x_err is set (the host
+// reports MEDHA_ENCCL) and the kernel finishes instead of hanging the GPU.
 template <int D, int G>
 __device__ __forceinline__ void xchg_merge_unit(const DecodeParams &p, const int unit, DecodeSmem<D, G> &sm) {
   const int tid = threadIdx.x;
+  const uint32_t epoch = sm.epoch;
   const int sidx = unit / p.h_kv, kvh = unit - sidx * p.h_kv;
+  char *local = p.x_peer[p.x_rank];
+  const uint32_t par = epoch & 1u;
+  const float *recv = xchg_slot(p, local, par, 0);
+  bool late = false;
   if (tid < p.x_world) {
-    const uint32_t *f = p.x_flags + (int64_t)tid * p.x_units + unit;
-    while (ld_acquire_sys(f) != p.x_epoch) {
+    const uint32_t *f = xchg_flags(p, local, par, tid) + unit;
+    if (ld_acquire_sys(f) != epoch) {
+      const unsigned long long t0 = global_ns();
+      unsigned spins = 0;
+      while (ld_acquire_sys(f) != epoch) {
+        if ((++spins & 255u) == 0 && global_ns() - t0 > p.x_timeout_ns) {
+          late = true;
+          break;
+        }
+      }
     }
   }
-  __syncthreads();
+  const int64_t obase = ((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D;
+  if (__syncthreads_or(late)) {
+    const float qnan = __int_as_float(0x7fc00000);
+    for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
+      p.x_o[obase + idx] = qnan;
+      if (p.x_obf) p.x_obf[obase + idx] = __float2bfloat16_rn(qnan);
+    }
+    if (tid < G && p.x_lse) p.x_lse[(int64_t)sidx * p.h_q + (int64_t)kvh * G + tid] = qnan;
+    if (tid == 0) atomicExch_system(p.x_err, 1u);
+    __syncthreads();
+    return;
+  }
   const int64_t lrow0 = p.x_rows * D + (int64_t)sidx * p.h_q + (int64_t)kvh * G;
   if (tid < G) {
     const int row = tid;
     float M = -INFINITY;
-    for (int r = 0; r < p.x_world; ++r) M = fmaxf(M, __ldcg(p.x_recv + (int64_t)r * p.x_slot + lrow0 + row));
+    for (int r = 0; r < p.x_world; ++r) M = fmaxf(M, __ldcg(recv + (int64_t)r * p.x_slot + lrow0 + row));
     float lse_f = -INFINITY;
     if (M != -INFINITY) {
       float ssum = 0.f;
-      for (int r = 0; r < p.x_world; ++r) ssum += __expf(__ldcg(p.x_recv + (int64_t)r * p.x_slot + lrow0 + row) - M);
+      for (int r = 0; r < p.x_world; ++r) ssum += __expf(__ldcg(recv + (int64_t)r * p.x_slot + lrow0 + row) - M);
       lse_f = M + __logf(ssum);
     }
     for (int r = 0; r < p.x_world; ++r)
-      sm.w[r * G + row] = (M == -INFINITY) ? 0.f : __expf(__ldcg(p.x_recv + (int64_t)r * p.x_slot + lrow0 + row) - lse_f);
+      sm.w[r * G + row] = (M == -INFINITY) ? 0.f : __expf(__ldcg(recv + (int64_t)r * p.x_slot + lrow0 + row) - lse_f);
     if (p.x_lse) p.x_lse[(int64_t)sidx * p.h_q + (int64_t)kvh * G + row] = lse_f;
   }
   __syncthreads();
-  const int64_t obase = ((int64_t)sidx * p.h_q + (int64_t)kvh * G) * D;
   for (int idx = tid; idx < G * D; idx += kDecodeThreads) {
     const int row = idx / D;
     float v[kMaxKvpRanks];
 #pragma unroll
-    for (int r = 0; r < kMaxKvpRanks; ++r) v[r] = (r < p.x_world) ? __ldcg(p.x_recv + (int64_t)r * p.x_slot + obase + idx) : 0.f;
+    for (int r = 0; r < kMaxKvpRanks; ++r) v[r] = (r < p.x_world) ? __ldcg(recv + (int64_t)r * p.x_slot + obase + idx) : 0.f;
     float o = 0.f;
 #pragma unroll
     for (int r = 0; r < kMaxKvpRanks; ++r)
@@ -571,6 +620,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
   // nothing is read or written before it has (KV rows, queue counters, outputs)
   pdl_wait();
   pdl_launch_dependents();
+  // fused exchange: this call's epoch = the last completed call's + 1 (same on every rank:
+  // each rank's word advances once per call of the collective)
+  if (threadIdx.x == 0) sm.epoch = (p.x_world > 0) ? *reinterpret_cast<volatile uint32_t *>(p.x_epoch) + 1u : 0u;
 #ifdef MEDHA_DECODE_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     g_ltrace[g_ltrace_n & 63][0] = t_entry;
@@ -597,6 +649,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
     if (atomicAdd(p.work + 1, 1u) == gridDim.x - 1) {
       p.work[0] = 0u;
       p.work[1] = 0u;
+      if (p.x_world > 0) *p.x_epoch = sm.epoch;   // every CTA has read it
       // device-length mode: every item has read the lengths; advance them for the next step
       for (int i = 0; i < p.n_seq; ++i)
         if (p.seq[i].len_dev) *p.seq[i].len_dev += 1;

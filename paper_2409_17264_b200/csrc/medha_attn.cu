@@ -191,12 +191,11 @@ medha_status dispatch_decode_g(int G, const DecodeParams &p, int grid, cudaStrea
 // Fused-exchange settings of one decode launch (see DecodeParams::x_*); null = off.
 struct DecodeXchg {
   int32_t world, rank, units;
-  uint32_t epoch;
+  uint32_t debug;
   int64_t rows, slot;
-  float *dst[kMaxKvpRanks];
-  uint32_t *flag_dst[kMaxKvpRanks];
-  const float *recv;
-  const uint32_t *flags;
+  uint64_t timeout_ns;
+  char *peer[kMaxKvpRanks];
+  uint32_t *epoch, *err;
   float *o, *lse;
   __nv_bfloat16 *obf;
 };
@@ -250,16 +249,14 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
     if (x) {
       p.x_world = x->world;
       p.x_rank = x->rank;
-      p.x_epoch = x->epoch;
       p.x_units = x->units;
+      p.x_debug = x->debug;
       p.x_rows = x->rows;
       p.x_slot = x->slot;
-      for (int r = 0; r < x->world; ++r) {
-        p.x_dst[r] = x->dst[r];
-        p.x_flag_dst[r] = x->flag_dst[r];
-      }
-      p.x_recv = x->recv;
-      p.x_flags = x->flags;
+      p.x_timeout_ns = x->timeout_ns;
+      for (int r = 0; r < x->world; ++r) p.x_peer[r] = x->peer[r];
+      p.x_epoch = x->epoch;
+      p.x_err = x->err;
       p.x_o = x->o;
       p.x_lse = x->lse;
       p.x_obf = x->obf;
@@ -417,11 +414,18 @@ size_t prefill_ws_bound(int64_t c, int32_t h_q, int32_t d) {
 template <int D, int G>
 medha_status launch_prefill(const PrefillBatch &b, int64_t items, cudaStream_t st) {
   using L = WsLayout<D>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(prefill_ws_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kAlloc));
-    attr_done = true;
-  }
+  // the dynamic shared memory opt-in is a per-device (context) attribute: set it once per
+  // device, thread-safely (std::call_once per device slot)
+  static std::once_flag once[64];
+  static cudaError_t attr_err[64];
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(MEDHA_ENOTSUP, "device ordinal %d >= 64", dev);
+  std::call_once(once[dev], [dev] {
+    attr_err[dev] = cudaFuncSetAttribute(prefill_ws_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)L::kAlloc);
+  });
+  CUDA_TRY(attr_err[dev]);
   launch_pdl(prefill_ws_kernel<D, G>, dim3((unsigned)items), dim3(kWsThreads), (size_t)L::kAlloc, st, b);
   LAUNCH_CHECK("prefill_ws_kernel");
   return MEDHA_OK;
@@ -559,8 +563,9 @@ medha_status prefill_impl(const medha_kv_shard *kv, const void *q, int64_t c, in
 struct medha_kvp_comm {
   ncclComm_t nccl;
   int32_t rank, world;
-  // fused P2P exchange (single node, CUDA IPC): one buffer per rank holding
-  // [2 parities][world src][slot floats] receive slots + [2][world][units] epoch flags
+  // fused P2P exchange (single node, CUDA IPC; at world 1 the local buffer alone): one
+  // buffer per rank holding [2 parities][world src][slot floats] receive slots +
+  // [2][world][units] epoch flags + the device epoch word (medha::XchgLayout below)
   bool p2p = false;
   bool p2p_on = false;      // runtime switch (medha_kvp_comm_set_p2p)
   int device = -1;
@@ -568,74 +573,73 @@ struct medha_kvp_comm {
   char *peer[kMaxKvpRanks] = {};  // every rank's buffer mapped here (peer[rank] = local)
   int64_t slot = 0;         // floats per (parity, src) slot
   int32_t units = 0;        // flags per (parity, src)
-  uint32_t epoch = 0;
+  void *agree = nullptr;    // device scratch of the set-up agreement (allocated before NCCL init)
+  uint32_t *err_host = nullptr;   // mapped pinned word the decode kernel sets on a timed-out wait
+  uint32_t *err_dev = nullptr;    // its device address
+  uint64_t timeout_ns = 0;
+  uint32_t debug = 0;       // test hook (medha_kvp_comm_debug)
+  bool broken = false;      // a fused wait timed out: every later collective call fails
 };
 
 namespace {
 constexpr int64_t kP2PSlotFloats = (int64_t)64 * 64 * 129;   // batch 64 x h_q 64 x (d 128 + 1)
 constexpr int32_t kP2PUnits = 4096;                           // (seq, kv head) units per call
+constexpr size_t kAgreeBytes = sizeof(cudaIpcMemHandle_t) * (kMaxKvpRanks + 1) + 256;
 
-size_t p2p_bytes(int world) {
-  return (size_t)2 * world * kP2PSlotFloats * sizeof(float) + (size_t)2 * world * kP2PUnits * sizeof(uint32_t);
-}
-float *p2p_slot(const medha_kvp_comm *c, char *base, int parity, int src) {
-  return reinterpret_cast<float *>(base) + ((int64_t)parity * c->world + src) * c->slot;
-}
-uint32_t *p2p_flags(const medha_kvp_comm *c, char *base, int parity, int src) {
-  return reinterpret_cast<uint32_t *>(base + (size_t)2 * c->world * c->slot * sizeof(float)) +
-         ((int64_t)parity * c->world + src) * c->units;
-}
+size_t p2p_flags_off(int world) { return (size_t)2 * world * kP2PSlotFloats * sizeof(float); }
+size_t p2p_epoch_off(int world) { return p2p_flags_off(world) + (size_t)2 * world * kP2PUnits * sizeof(uint32_t); }
+size_t p2p_bytes(int world) { return p2p_epoch_off(world) + 256; }
 
 // Collective: allocate the receive buffer, exchange CUDA IPC handles with ncclAllGather
-// and map every peer's buffer.  Any failure leaves the communicator on the NCCL path.
+// and map every peer's buffer.  Every rank takes part in both agreement all-reduces
+// whatever fails locally, and any failure leaves the communicator on the NCCL path.
+// World 1: the local buffer alone (the kernel's push, flags and merge run as a self-loop).
 void p2p_setup(medha_kvp_comm *c) {
-  if (c->world < 2 || c->world > kMaxKvpRanks || getenv_flag("MEDHA_KVP_P2P", 1) == 0) return;
-  cudaStream_t st;
-  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return;
+  if (c->world > kMaxKvpRanks || getenv_flag("MEDHA_KVP_P2P", 1) == 0 || !c->agree || !c->err_dev) return;
   const size_t bytes = p2p_bytes(c->world);
-  cudaIpcMemHandle_t *hs = nullptr;
-  cudaIpcMemHandle_t mine;
   int ok = 1;
-  void *dbuf = nullptr;
-  int *dok = nullptr;
-  if (cudaMalloc(&c->local, bytes) != cudaSuccess || cudaMemset(c->local, 0, bytes) != cudaSuccess ||
-      cudaIpcGetMemHandle(&mine, c->local) != cudaSuccess)
-    ok = 0;
-  // agree on success everywhere (a partial setup would deadlock the fused kernels)
-  if (cudaMalloc(&dbuf, sizeof(cudaIpcMemHandle_t) * (c->world + 1)) != cudaSuccess) ok = 0;
-  if (cudaMalloc(&dok, sizeof(int)) != cudaSuccess) {
-    cudaFree(dbuf);
-    cudaStreamDestroy(st);
-    if (c->local) cudaFree(c->local);
-    c->local = nullptr;
-    return;
-  }
-  cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice);
-  ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, c->nccl, st);
-  cudaStreamSynchronize(st);
-  cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost);
-  if (ok) {
-    char *slots = static_cast<char *>(dbuf);
-    cudaMemcpy(slots + sizeof(cudaIpcMemHandle_t) * c->world, &mine, sizeof(mine), cudaMemcpyHostToDevice);
-    ncclAllGather(slots + sizeof(cudaIpcMemHandle_t) * c->world, slots, sizeof(cudaIpcMemHandle_t), ncclChar,
-                  c->nccl, st);
-    cudaStreamSynchronize(st);
-    hs = new cudaIpcMemHandle_t[c->world];
-    cudaMemcpy(hs, slots, sizeof(cudaIpcMemHandle_t) * c->world, cudaMemcpyDeviceToHost);
-    for (int r = 0; r < c->world; ++r) {
-      if (r == c->rank) {
-        c->peer[r] = c->local;
-        continue;
-      }
-      void *ptr = nullptr;
-      if (cudaIpcOpenMemHandle(&ptr, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) ok = 0;
-      c->peer[r] = static_cast<char *>(ptr);
+  if (cudaMalloc(&c->local, bytes) != cudaSuccess || cudaMemset(c->local, 0, bytes) != cudaSuccess) ok = 0;
+  if (c->world == 1) {
+    if (ok) {
+      cudaDeviceSynchronize();
+      c->peer[0] = c->local;
     }
-    cudaGetLastError();
-    cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice);
-    ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, c->nccl, st);
-    cudaStreamSynchronize(st);
-    cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost);
+  } else {
+    cudaStream_t st = nullptr;
+    cudaIpcMemHandle_t mine;
+    memset(&mine, 0, sizeof(mine));
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) st = nullptr;
+    if (!ok || !st || cudaIpcGetMemHandle(&mine, c->local) != cudaSuccess) ok = 0;
+    char *slots = static_cast<char *>(c->agree);
+    int *dok = reinterpret_cast<int *>(slots + sizeof(cudaIpcMemHandle_t) * (kMaxKvpRanks + 1));
+    auto agree = [&](int v) {   // collective min over ranks (every rank calls it)
+      cudaMemcpy(dok, &v, sizeof(int), cudaMemcpyHostToDevice);
+      ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, c->nccl, st);
+      cudaStreamSynchronize(st);
+      cudaMemcpy(&v, dok, sizeof(int), cudaMemcpyDeviceToHost);
+      return v;
+    };
+    ok = agree(ok);
+    if (ok) {
+      cudaMemcpy(slots + sizeof(cudaIpcMemHandle_t) * kMaxKvpRanks, &mine, sizeof(mine), cudaMemcpyHostToDevice);
+      ncclAllGather(slots + sizeof(cudaIpcMemHandle_t) * kMaxKvpRanks, slots, sizeof(cudaIpcMemHandle_t), ncclChar,
+                    c->nccl, st);
+      cudaStreamSynchronize(st);
+      std::vector<cudaIpcMemHandle_t> hs(c->world);
+      cudaMemcpy(hs.data(), slots, sizeof(cudaIpcMemHandle_t) * c->world, cudaMemcpyDeviceToHost);
+      for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) {
+          c->peer[r] = c->local;
+          continue;
+        }
+        void *ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) ok = 0;
+        c->peer[r] = static_cast<char *>(ptr);
+      }
+      cudaGetLastError();
+      ok = agree(ok);
+    }
+    if (st) cudaStreamDestroy(st);
   }
   if (ok) {
     c->slot = kP2PSlotFloats;
@@ -648,11 +652,18 @@ void p2p_setup(medha_kvp_comm *c) {
     c->local = nullptr;
     for (int r = 0; r < kMaxKvpRanks; ++r) c->peer[r] = nullptr;
   }
-  delete[] hs;
-  cudaFree(dbuf);
-  cudaFree(dok);
-  cudaStreamDestroy(st);
   cudaGetLastError();
+}
+
+// Sticky health of a communicator: a fused wait that timed out (set by the kernel in mapped
+// host memory, read here without synchronising) marks it broken for good.
+medha_status comm_health(medha_kvp_comm *c) {
+  if (!c->broken && c->err_host && *reinterpret_cast<volatile uint32_t *>(c->err_host) != 0u) c->broken = true;
+  if (c->broken)
+    return fail(MEDHA_ENCCL,
+                "KVP communicator unusable: a fused-exchange wait timed out (a rank did not join a collective "
+                "call, or ranks disagree on its arguments); destroy and re-create it");
+  return MEDHA_OK;
 }
 }  // namespace
 
@@ -792,12 +803,30 @@ medha_status medha_kvp_comm_create(const uint8_t id[128], int32_t rank, int32_t 
   medha_kvp_comm *c = new medha_kvp_comm();
   c->rank = rank;
   c->world = world;
+  c->timeout_ns = (uint64_t)std::max(1, getenv_flag("MEDHA_KVP_TIMEOUT_MS", 30000)) * 1000000ull;
+  cudaGetDevice(&c->device);
+  // local resources the set-up needs are taken BEFORE the collective NCCL init, so a rank
+  // that cannot get them fails before any peer is waiting on it inside a collective
+  void *eh = nullptr;
+  if (cudaMalloc(&c->agree, kAgreeBytes) != cudaSuccess ||
+      cudaHostAlloc(&eh, 256, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    if (c->agree) cudaFree(c->agree);
+    delete c;
+    return fail(MEDHA_ECUDA, "kvp_comm_create: device/host allocation failed");
+  }
+  c->err_host = static_cast<uint32_t *>(eh);
+  *c->err_host = 0u;
+  void *ed = nullptr;
+  if (cudaHostGetDevicePointer(&ed, eh, 0) == cudaSuccess) c->err_dev = static_cast<uint32_t *>(ed);
+  cudaGetLastError();
   ncclResult_t r = ncclCommInitRank(&c->nccl, world, uid, rank);
   if (r != ncclSuccess) {
+    cudaFree(c->agree);
+    cudaFreeHost(eh);
     delete c;
     return fail(MEDHA_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
   }
-  cudaGetDevice(&c->device);
   p2p_setup(c);
   *out = c;
   return MEDHA_OK;
@@ -805,15 +834,35 @@ medha_status medha_kvp_comm_create(const uint8_t id[128], int32_t rank, int32_t 
 
 medha_status medha_kvp_comm_destroy(medha_kvp_comm *comm) {
   if (!comm) return MEDHA_OK;
+  cudaDeviceSynchronize();
   if (comm->p2p) {
-    cudaDeviceSynchronize();
     for (int r = 0; r < comm->world; ++r)
       if (r != comm->rank && comm->peer[r]) cudaIpcCloseMemHandle(comm->peer[r]);
     cudaFree(comm->local);
   }
-  ncclResult_t r = ncclCommDestroy(comm->nccl);
+  if (comm->agree) cudaFree(comm->agree);
+  if (comm->err_host) cudaFreeHost(comm->err_host);
+  ncclResult_t r = comm->broken ? ncclCommAbort(comm->nccl) : ncclCommDestroy(comm->nccl);
   delete comm;
   if (r != ncclSuccess) return fail(MEDHA_ENCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+  return MEDHA_OK;
+}
+
+medha_status medha_kvp_comm_status(medha_kvp_comm *comm) {
+  if (!comm) return fail(MEDHA_EINVAL, "null comm");
+  return comm_health(comm);
+}
+
+medha_status medha_kvp_comm_set_timeout(medha_kvp_comm *comm, uint64_t timeout_ns) {
+  if (!comm) return fail(MEDHA_EINVAL, "null comm");
+  if (timeout_ns == 0) return fail(MEDHA_EINVAL, "timeout must be > 0");
+  comm->timeout_ns = timeout_ns;
+  return MEDHA_OK;
+}
+
+medha_status medha_kvp_comm_debug(medha_kvp_comm *comm, uint32_t flags) {
+  if (!comm) return fail(MEDHA_EINVAL, "null comm");
+  comm->debug = flags;
   return MEDHA_OK;
 }
 
@@ -859,6 +908,7 @@ medha_status medha_kvp_exchange_merge(medha_kvp_comm *comm, const float *send, i
                                       float *lse_out, void *o_out_bf16, void *ws, size_t ws_bytes, void *stream) {
   if (!comm || !send || !o_out) return fail(MEDHA_EINVAL, "null argument");
   if (rows <= 0) return fail(MEDHA_EINVAL, "rows must be > 0");
+  if (medha_status h = comm_health(comm)) return h;
   if (!supported_d(d)) return fail(MEDHA_ENOTSUP, "head dim %d", d);
   const size_t need = medha_kvp_exchange_workspace_size(comm->world, rows, d);
   if (!ws || ws_bytes < need) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
@@ -868,13 +918,14 @@ medha_status medha_kvp_exchange_merge(medha_kvp_comm *comm, const float *send, i
 
 size_t medha_kvp_workspace_size(int32_t world, int32_t batch, int32_t h_q, int32_t h_kv, int32_t d) {
   if (world < 1 || batch <= 0 || h_q <= 0 || d <= 0) return 256;
-  return kvp_buf_bytes(world, (int64_t)batch * h_q, d) + medha_decode_workspace_size(batch, h_q, h_kv, d);
+  return kvp_buf_bytes(world, (int64_t)batch * h_q, d) + round_up(medha_decode_workspace_size(batch, h_q, h_kv, d), 256);
 }
 
 medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_host, int32_t batch, const void *q,
                               int32_t h_q, const int64_t *q_pos_host, float scale, float *o_out, float *lse_out,
                               void *o_out_bf16, void *ws, size_t ws_bytes, void *stream) {
   if (!comm) return fail(MEDHA_EINVAL, "null comm");
+  if (medha_status h = comm_health(comm)) return h;
   if (batch <= 0 || !kvs_host) return fail(MEDHA_EINVAL, "empty batch");
   if (!o_out) return fail(MEDHA_EINVAL, "null o_out");
   const int32_t d = kvs_host[0].d, h_kv = kvs_host[0].h_kv;
@@ -883,37 +934,38 @@ medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_ho
   const size_t need = medha_kvp_workspace_size(comm->world, batch, h_q, h_kv, d);
   if (!ws || ws_bytes < need) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // the decode workspace (its zeroed counter block first) sits at offset 0 whatever the call
+  // shape, so one workspace serves calls of different shapes; send / recv follow it
   char *base = static_cast<char *>(ws);
   const size_t count = (size_t)rows * (d + 1);
-  float *send = reinterpret_cast<float *>(base);
-  float *recv = reinterpret_cast<float *>(base + round_up(count * 4, 256));
-  char *dws = base + kvp_buf_bytes(comm->world, rows, d);
+  char *dws = base;
+  const size_t dws_bytes = round_up(medha_decode_workspace_size(batch, h_q, h_kv, d), 256);
+  float *send = reinterpret_cast<float *>(base + dws_bytes);
+  float *recv = reinterpret_cast<float *>(base + dws_bytes + round_up(count * 4, 256));
   if (comm->p2p && comm->p2p_on && batch <= kDecodeMaxSeqPerLaunch && (int64_t)count <= comm->slot &&
       (int64_t)batch * h_kv <= comm->units) {
-    // fused: the decode kernel's last CTAs push the partials over NVLink and merge
+    // fused: the decode kernel's last CTAs push the partials over NVLink and merge; the
+    // epoch and the slot parity are resolved on the device (graph-replayable)
     DecodeXchg x;
     memset(&x, 0, sizeof(x));
     x.world = comm->world;
     x.rank = comm->rank;
-    x.epoch = ++comm->epoch;
     x.units = comm->units;
     x.rows = rows;
     x.slot = comm->slot;
-    const int par = (int)(x.epoch & 1u);
-    for (int r = 0; r < comm->world; ++r) {
-      x.dst[r] = p2p_slot(comm, comm->peer[r], par, comm->rank);
-      x.flag_dst[r] = p2p_flags(comm, comm->peer[r], par, comm->rank);
-    }
-    x.recv = p2p_slot(comm, comm->local, par, 0);
-    x.flags = p2p_flags(comm, comm->local, par, 0);
+    x.debug = comm->debug;
+    x.timeout_ns = comm->timeout_ns;
+    for (int r = 0; r < comm->world; ++r) x.peer[r] = comm->peer[r];
+    x.epoch = reinterpret_cast<uint32_t *>(comm->local + p2p_epoch_off(comm->world));
+    x.err = comm->err_dev;
     x.o = o_out;
     x.lse = lse_out;
     x.obf = static_cast<__nv_bfloat16 *>(o_out_bf16);
     return decode_partial_impl(kvs_host, batch, q, h_q, q_pos_host, scale, o_out, send + rows * d, dws,
-                               ws_bytes - (size_t)(dws - base), st, &x);
+                               dws_bytes, st, &x);
   }
   medha_status s = decode_partial_impl(kvs_host, batch, q, h_q, q_pos_host, scale, send, send + rows * d, dws,
-                                       ws_bytes - (size_t)(dws - base), st);
+                                       dws_bytes, st);
   if (s) return s;
   return kvp_exchange_merge(comm, send, recv, rows, d, o_out, lse_out, o_out_bf16, st);
 }
@@ -927,6 +979,7 @@ medha_status medha_kvp_prefill_chunk(medha_kvp_comm *comm, const medha_kv_shard 
                                      int32_t h_q, int64_t q_pos0, float scale, float *o_out, float *lse_out,
                                      void *o_out_bf16, void *ws, size_t ws_bytes, void *stream) {
   if (!comm) return fail(MEDHA_EINVAL, "null comm");
+  if (medha_status h = comm_health(comm)) return h;
   if (!kv) return fail(MEDHA_EINVAL, "null shard");
   if (c <= 0) return fail(MEDHA_EINVAL, "empty chunk");
   if (!o_out) return fail(MEDHA_EINVAL, "null o_out");
@@ -952,8 +1005,8 @@ size_t medha_decode_step_workspace_size(int32_t world, int32_t h_q, int32_t h_kv
   if (h_q <= 0 || h_kv <= 0 || d <= 0) return 256;
   const size_t stage = round_up((size_t)h_q * d * 2, 256) + 2 * round_up((size_t)h_kv * d * 2, 256) +
                        round_up((size_t)h_q * d * 4, 256) + round_up((size_t)h_q * 4, 256);
-  const size_t inner = world > 1 ? medha_kvp_workspace_size(world, 1, h_q, h_kv, d)
-                                 : medha_decode_workspace_size(1, h_q, h_kv, d);
+  // sized for the KVP call (a world-1 communicator included); >= the plain decode's
+  const size_t inner = round_up(medha_kvp_workspace_size(std::max(world, 1), 1, h_q, h_kv, d), 256);
   return stage + inner;
 }
 
@@ -970,7 +1023,11 @@ medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, in
   const size_t need = medha_decode_step_workspace_size(world, h_q, h_kv, d);
   if (!ws || ws_bytes < need) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  char *b = static_cast<char *>(ws);
+  // the inner (decode / KVP) workspace first: its counter block stays at offset 0 for any
+  // shape; the staging buffers follow it
+  const size_t inner_bytes = round_up(medha_kvp_workspace_size(std::max(world, 1), 1, h_q, h_kv, d), 256);
+  char *inner = static_cast<char *>(ws);
+  char *b = inner + inner_bytes;
   const size_t qb = (size_t)h_q * d * 2, kb = (size_t)h_kv * d * 2;
   void *q_dev = b;
   b += round_up(qb, 256);
@@ -982,7 +1039,6 @@ medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, in
   b += round_up((size_t)h_q * d * 4, 256);
   float *lse_dev = reinterpret_cast<float *>(b);
   b += round_up((size_t)h_q * 4, 256);
-  const size_t rest = ws_bytes - (size_t)(b - static_cast<char *>(ws));
   // Inputs: with mapped pinned host buffers, ONE launch reads q, k_new and v_new over the
   // host link (q into the workspace, K/V appended straight into the shard); otherwise three
   // cudaMemcpyAsync + kv_append.
@@ -1011,9 +1067,9 @@ medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, in
   float *l_tgt = zc_out ? (lse_host ? l_map : lse_dev) : lse_dev;
   const int64_t qp = q_pos;
   if (comm)
-    s = medha_kvp_decode(comm, kv, 1, q_dev, h_q, &qp, scale, o_tgt, l_tgt, nullptr, b, rest, stream);
+    s = medha_kvp_decode(comm, kv, 1, q_dev, h_q, &qp, scale, o_tgt, l_tgt, nullptr, inner, inner_bytes, stream);
   else
-    s = decode_partial_impl(kv, 1, q_dev, h_q, &qp, scale, o_tgt, l_tgt, b, rest, st);
+    s = decode_partial_impl(kv, 1, q_dev, h_q, &qp, scale, o_tgt, l_tgt, inner, inner_bytes, st);
   if (s) return s;
   if (!zc_out) {
     CUDA_TRY(cudaMemcpyAsync(o_host, o_dev, (size_t)h_q * d * 4, cudaMemcpyDeviceToHost, st));
