@@ -195,24 +195,25 @@ def bench_decode(args, rank, world, M):
     ev_every = EV_EVERY if args.steps >= 2 * EV_EVERY else 1
 
     def step(i=None):
+        # ONE launch per step and rank: the tail rank's append of the new token rides in the
+        # decode launch (medha_attn_decode_append / medha_kvp_decode_append)
         if tail:
             sh.len = len_before
-            M.kv_append(sh, k_new, v_new)
         e = ev[i] if (i is not None and i % ev_every == ev_every - 1) else None
         if e:
             e[0].record(stream)
         if world == 1:
-            M.attn_decode_partial([sh], q, [new_pos], o=o_out, lse=lse_out, ws=dws)
+            M.attn_decode_append([sh], k_new, v_new, q, [new_pos], o=o_out, lse=lse_out, ws=dws)
             if e:
                 e[1].record(stream)
         elif comm.p2p:
-            # one launch: decode partial + NVLink push + rank-ordered merge (fused exchange)
-            M.kvp_decode(comm, [sh], q, [new_pos], ws=kws, o=o_out, lse=lse_out)
+            # decode partial + append + NVLink push + rank-ordered merge (fused exchange)
+            M.kvp_decode_append(comm, [sh], k_new, v_new, q, [new_pos], append=[tail], ws=kws, o=o_out, lse=lse_out)
             if e:
                 e[1].record(stream)
         else:
-            M.attn_decode_partial([sh], q, [new_pos], o=parts_send[:rows * D].view(1, H_Q, D),
-                                  lse=parts_send[rows * D:].view(1, H_Q), ws=dws)
+            o_p, l_p = parts_send[:rows * D].view(1, H_Q, D), parts_send[rows * D:].view(1, H_Q)
+            M.attn_decode_append([sh], k_new, v_new, q, [new_pos], append=[tail], o=o_p, lse=l_p, ws=dws)
             if e:
                 e[1].record(stream)
             M.kvp_exchange_merge(comm, parts_send, rows, D, o_out, lse_out, ws=xws)
@@ -276,7 +277,7 @@ def bench_decode(args, rank, world, M):
     h2d = world * (H_Q * D * 2) + 2 * H_KV * D * 2
     d2h = world * (H_Q * D * 4 + H_Q * 4)
     fused = comm is not None and comm.p2p
-    launches_per_step = (2 if tail else 1) + (1 if (world > 1 and not fused) else 0)   # rank-0 view
+    launches_per_step = 1 + (1 if (world > 1 and not fused) else 0)   # rank-0 view (NCCL path: + merge kernel)
     exch = "none" if comm is None else ("fused NVLink push in the decode kernel" if fused else "NCCL all-gather + merge kernel")
     if comm is not None:
         comm.close()
@@ -329,7 +330,7 @@ def bench_graph_decode(M, iters=50, warm=5):
     del sh
     torch.cuda.empty_cache()
     return {"ms_per_step": round(ms, 5), "GBps": round(N_KV * H_KV * D * 2 * 2 / (ms * 1e-3) / 1e9, 1),
-            "graph": "length reset (memcpy) + kv_append_dev + decode, replayed", "replays": iters,
+            "graph": "length reset (memcpy) + one decode launch with the fused append, replayed", "replays": iters,
             "output_equals_eager_call": same}
 
 

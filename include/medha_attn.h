@@ -126,6 +126,22 @@ medha_status medha_attn_decode_partial(const medha_kv_shard *kvs_host, int32_t b
                                        void *ws, size_t ws_bytes, void *stream);
 
 /*
+ * attn_decode_append (SURVEY a1 + a3 + a5 in ONE launch; P:178-183 each decode step appends
+ * one K/V row per sequence and then scans the whole KV): exactly medha_kv_append of row b of
+ * k_new / v_new (device, bf16 [batch][h_kv][d], token-major) into shard kvs_host[b] followed
+ * by medha_attn_decode_partial, for every sequence b with append_host[b] != 0 (append_host ==
+ * NULL: every sequence).  The kernel item whose KV split owns the new token stores its rows;
+ * every read of that token takes it from k_new / v_new, so no CTA reads data another CTA
+ * wrote in the same launch.  On success kvs_host[b].len += 1 for the appending sequences.
+ * Errors as medha_attn_decode_partial, plus MEDHA_ERANGE when an append would exceed a
+ * shard's capacity (nothing is launched).
+ */
+medha_status medha_attn_decode_append(medha_kv_shard *kvs_host, int32_t batch, const void *k_new,
+                                      const void *v_new, const int32_t *append_host, const void *q,
+                                      int32_t h_q, const int64_t *q_pos_host, float scale, float *o,
+                                      float *lse, void *ws, size_t ws_bytes, void *stream);
+
+/*
  * attn_prefill_chunk (P:321-366 chunked prefill, Eq. 3): a chunk of c
  * query tokens q (bf16 [c][h_q][d]) at absolute positions q_pos0 .. q_pos0+c-1
  * attends causally over the shard `kv` (all of its len tokens that are visible).
@@ -237,6 +253,17 @@ medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_ho
                               void *ws, size_t ws_bytes, void *stream);
 
 /*
+ * kvp_decode_append: medha_kvp_decode with the new token's K/V appended in the same launch on
+ * the ranks / sequences that hold it (append_host[b] != 0; typically the tail rank of each
+ * sequence), as medha_attn_decode_append.  kvs_host[b].len += 1 where appended.
+ */
+medha_status medha_kvp_decode_append(medha_kvp_comm *comm, medha_kv_shard *kvs_host, int32_t batch,
+                                     const void *k_new, const void *v_new, const int32_t *append_host,
+                                     const void *q, int32_t h_q, const int64_t *q_pos_host, float scale,
+                                     float *o_out, float *lse_out, void *o_out_bf16, void *ws,
+                                     size_t ws_bytes, void *stream);
+
+/*
  * kvp_exchange_merge (SURVEY a6 + a7 on their own): all-gathers this rank's packed
  * partial `send` (fp32 [rows*(d+1)]: o [rows][d] then lse [rows], e.g. written by
  * medha_attn_decode_partial with o = send, lse = send + rows*d) and merges the
@@ -289,6 +316,8 @@ medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, in
  * `batch` (1..64) sequences on this GPU, all lengths on the DEVICE:
  *   1. k_new / v_new (bf16 [batch][h_kv][d], device) row b is appended to shard b at local
  *      index len_dev[b] (int64 [batch], device; appends at or past the capacity are dropped);
+ *      the append runs inside the decode launch (one launch per step, as
+ *      medha_attn_decode_append);
  *   2. sequence b attends keys 0..len_dev[b] of its shard (its own new token included; the
  *      query is q[b], bf16 [batch][h_q][d], at position pos0 + len_dev[b]) -> o fp32
  *      [batch][h_q][d], lse fp32 [batch][h_q] (natural log);

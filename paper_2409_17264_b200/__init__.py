@@ -19,7 +19,8 @@ from typing import List, Optional, Sequence
 
 import torch
 
-__all__ = ["lib", "MedhaError", "KVShard", "kv_append", "attn_decode_partial", "attn_prefill_chunk",
+__all__ = ["lib", "MedhaError", "KVShard", "kv_append", "attn_decode_partial", "attn_decode_append",
+           "kvp_decode_append", "attn_prefill_chunk",
            "merge_partials", "KVPComm", "kvp_decode", "kvp_exchange_merge", "exchange_workspace", "kvp_prefill_chunk", "decode_step_host",
            "hbm_read_probe", "decode_workspace", "prefill_workspace", "kvp_workspace", "LIB_PATH"]
 
@@ -77,6 +78,9 @@ _sig("medha_kvp_prefill_chunk", _i32, _vp, _P(_Shard), _vp, _i64, _i32, _i64, _f
 _sig("medha_decode_step_workspace_size", _sz, _i32, _i32, _i32, _i32)
 _sig("medha_decode_step_host", _i32, _vp, _P(_Shard), _i32, _vp, _vp, _vp, _i32, _i64, _f32, _vp, _vp, _vp, _sz,
      _vp)
+_sig("medha_attn_decode_append", _i32, _P(_Shard), _i32, _vp, _vp, _vp, _vp, _i32, _P(_i64), _f32, _vp, _vp, _vp, _sz, _vp)
+_sig("medha_kvp_decode_append", _i32, _vp, _P(_Shard), _i32, _vp, _vp, _vp, _vp, _i32, _P(_i64), _f32, _vp, _vp, _vp,
+     _vp, _sz, _vp)
 _sig("medha_decode_step_dev", _i32, _P(_Shard), _i32, _vp, _vp, _vp, _i32, _vp, _f32, _vp, _vp, _vp, _sz, _vp)
 _sig("medha_hbm_read_probe", _i32, _vp, _sz, _vp, _vp)
 
@@ -223,6 +227,42 @@ def attn_decode_partial(shards: Sequence[KVShard], q: torch.Tensor, q_pos: Seque
     qp = (ctypes.c_int64 * B)(*[int(x) for x in q_pos])
     _check(lib.medha_attn_decode_partial(_shards_c(shards), B, _ptr(q), h_q, qp, _scale(scale, d), _ptr(o),
                                          _ptr(lse), _ptr(ws), ws.numel(), _stream(stream)), "attn_decode_partial")
+    return o, lse
+
+
+def _append_mask(shards, append):
+    if append is None:
+        return None
+    if len(append) != len(shards):
+        raise ValueError("need one append flag per sequence")
+    return (ctypes.c_int32 * len(shards))(*[1 if a else 0 for a in append])
+
+
+def attn_decode_append(shards: Sequence[KVShard], k_new: torch.Tensor, v_new: torch.Tensor, q: torch.Tensor,
+                       q_pos: Sequence[int], append: Optional[Sequence[bool]] = None, scale=None,
+                       o: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
+                       ws: Optional[torch.Tensor] = None, stream=None):
+    """K1 + K3 + K4 in one launch: append row b of k_new / v_new (bf16 [B][h_kv][d]) to
+    shards[b] (where append[b], default all) and decode; shard.len advances."""
+    _need_cuda(q, "q", torch.bfloat16)
+    _need_cuda(k_new, "k_new", torch.bfloat16)
+    _need_cuda(v_new, "v_new", torch.bfloat16)
+    B, h_q, d = q.shape
+    if len(shards) != B or len(q_pos) != B:
+        raise ValueError("need one shard and one q_pos per sequence")
+    if o is None:
+        o = torch.empty((B, h_q, d), dtype=torch.float32, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, h_q), dtype=torch.float32, device=q.device)
+    if ws is None:
+        ws = decode_workspace(B, h_q, shards[0].h_kv, d, q.device, stream)
+    arr = _shards_c(shards)
+    qp = (ctypes.c_int64 * B)(*[int(x) for x in q_pos])
+    _check(lib.medha_attn_decode_append(arr, B, _ptr(k_new), _ptr(v_new), _append_mask(shards, append), _ptr(q), h_q,
+                                        qp, _scale(scale, d), _ptr(o), _ptr(lse), _ptr(ws), ws.numel(),
+                                        _stream(stream)), "attn_decode_append")
+    for i, sh in enumerate(shards):
+        sh.len = arr[i].len
     return o, lse
 
 
@@ -373,6 +413,32 @@ def kvp_decode(comm: KVPComm, shards: Sequence[KVShard], q: torch.Tensor, q_pos:
     qp = (ctypes.c_int64 * B)(*[int(x) for x in q_pos])
     _check(lib.medha_kvp_decode(comm.handle, _shards_c(shards), B, _ptr(q), h_q, qp, _scale(scale, d), _ptr(o),
                                 _ptr(lse), _ptr(ob), _ptr(ws), ws.numel(), _stream(stream)), "kvp_decode")
+    return o, lse, ob
+
+
+def kvp_decode_append(comm: KVPComm, shards: Sequence[KVShard], k_new: torch.Tensor, v_new: torch.Tensor,
+                      q: torch.Tensor, q_pos: Sequence[int], append: Optional[Sequence[bool]] = None, scale=None,
+                      want_bf16=False, ws=None, stream=None, o=None, lse=None):
+    """kvp_decode with the new token appended in the same launch where append[b] (default
+    all; typically this rank holds sequence b's tail)."""
+    _need_cuda(q, "q", torch.bfloat16)
+    _need_cuda(k_new, "k_new", torch.bfloat16)
+    _need_cuda(v_new, "v_new", torch.bfloat16)
+    B, h_q, d = q.shape
+    if o is None:
+        o = torch.empty((B, h_q, d), dtype=torch.float32, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, h_q), dtype=torch.float32, device=q.device)
+    ob = torch.empty((B, h_q, d), dtype=torch.bfloat16, device=q.device) if want_bf16 else None
+    if ws is None:
+        ws = kvp_workspace(comm.world, B, h_q, shards[0].h_kv, d, q.device, stream)
+    arr = _shards_c(shards)
+    qp = (ctypes.c_int64 * B)(*[int(x) for x in q_pos])
+    _check(lib.medha_kvp_decode_append(comm.handle, arr, B, _ptr(k_new), _ptr(v_new), _append_mask(shards, append),
+                                       _ptr(q), h_q, qp, _scale(scale, d), _ptr(o), _ptr(lse), _ptr(ob), _ptr(ws),
+                                       ws.numel(), _stream(stream)), "kvp_decode_append")
+    for i, sh in enumerate(shards):
+        sh.len = arr[i].len
     return o, lse, ob
 
 

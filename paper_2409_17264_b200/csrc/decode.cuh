@@ -83,6 +83,14 @@ struct DecodeSeq {
   int64_t n_vis;         // visible local tokens (keys 0..n_vis-1); with len_dev: an upper bound
   int64_t *len_dev;       // device-length mode (graph-capturable step): keys 0..*len_dev are
                           // visible (the token appended at *len_dev included), *len_dev += 1 at the end
+  // fused kv_append (SURVEY a1 in the decode launch): the new token's rows [h_kv][D] (bf16,
+  // 16-byte vectors) go to local index t_app (len_dev mode: *len_dev; dropped at or past the
+  // capacity).  The item whose split owns t_app writes them into the shard; every load of
+  // token t_app reads k_app / v_app instead, so no CTA reads back what another wrote.
+  const uint4 *k_app;     // null: no append
+  const uint4 *v_app;
+  int64_t t_app;
+  int64_t cap;            // capacity (logical tokens) of the shard
   int32_t split_tokens;  // tokens per split, multiple of 64
   int32_t n_splits;      // splits per kv head
   int32_t cta_begin;     // first CTA of this sequence (CTAs ordered [kvh][split])
@@ -189,6 +197,12 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   // o = 0, lse = -inf, which the split merge ignores)
   const int64_t n_vis = S.len_dev ? min64(S.n_vis, *S.len_dev + 1) : S.n_vis;
   const int64_t t_end = min64(t_begin + S.split_tokens, n_vis);
+  // fused append: token t_app (-1: none) comes from k_app / v_app
+  int64_t t_app = -1;
+  if (S.k_app) {
+    t_app = S.len_dev ? *S.len_dev : S.t_app;
+    if (t_app >= S.cap) t_app = -1;
+  }
 
   const __nv_bfloat16 *kbase = S.k + (int64_t)kvh * S.hstride * D;
   const __nv_bfloat16 *vbase = S.v + (int64_t)kvh * S.hstride * D;
@@ -222,13 +236,15 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   float m_lo = -INFINITY, m_hi = -INFINITY;  // running max (base 2) of rows g, g+8
   float l_lo = 0.f, l_hi = 0.f;              // thread-partial running sums
 
+  const __nv_bfloat16 *kapp = S.k_app ? reinterpret_cast<const __nv_bfloat16 *>(S.k_app) + (int64_t)kvh * D : nullptr;
+  const __nv_bfloat16 *vapp = S.v_app ? reinterpret_cast<const __nv_bfloat16 *>(S.v_app) + (int64_t)kvh * D : nullptr;
   auto load_tile = [&](int64_t tb, uint4 (&kk)[2][KCH], uint4 (&vv)[4][VCH]) {
     const int64_t row0 = tile_row(tb);
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       const int64_t tok = tb + 8 * n + g;
       const bool ok = tok < t_end;
-      const __nv_bfloat16 *src = kbase + (row0 + 8 * n + g) * D + 8 * c;
+      const __nv_bfloat16 *src = (tok == t_app) ? kapp + 8 * c : kbase + (row0 + 8 * n + g) * D + 8 * c;
 #pragma unroll
       for (int i = 0; i < KCH; ++i) kk[n][i] = ok ? ldg_stream(src + 32 * i) : make_uint4(0, 0, 0, 0);
     }
@@ -236,7 +252,8 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
     for (int r = 0; r < 4; ++r) {
       const int64_t tok = tb + 2 * c + (r & 1) + 8 * (r >> 1);
       const bool ok = tok < t_end;
-      const __nv_bfloat16 *src = vbase + (row0 + 2 * c + (r & 1) + 8 * (r >> 1)) * D + 8 * g;
+      const __nv_bfloat16 *src =
+          (tok == t_app) ? vapp + 8 * g : vbase + (row0 + 2 * c + (r & 1) + 8 * (r >> 1)) * D + 8 * g;
 #pragma unroll
       for (int i = 0; i < VCH; ++i) vv[r][i] = ok ? ldg_stream(src + 64 * i) : make_uint4(0, 0, 0, 0);
     }
@@ -337,6 +354,14 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
     }
   };
 
+  // the owner of t_app (its split, or the last split when t_app lies past the visible keys)
+  // stores the new K / V rows of this kv head into the shard (never read back in this launch)
+  if (t_app >= 0 && split == (int)min64(t_app / S.split_tokens, S.n_splits - 1) && tid < 2 * (D / 8)) {
+    const int64_t row = tile_row(t_app & ~15ll) + (t_app & 15);
+    const int e = tid % (D / 8);
+    uint4 *dst = reinterpret_cast<uint4 *>(const_cast<__nv_bfloat16 *>(tid < D / 8 ? kbase : vbase) + row * D) + e;
+    *dst = (tid < D / 8 ? S.k_app : S.v_app)[(int64_t)kvh * (D / 8) + e];
+  }
   MEDHA_TRACE(0);
   constexpr int64_t kStep = 16 * kDecodeWarps;
   int64_t tb = t_begin + 16 * warp;

@@ -202,10 +202,19 @@ struct DecodeXchg {
 
 // len_dev (device-length mode, medha_decode_step_dev): q_pos unused; sequence b attends keys
 // 0..len_dev[b] read at run time, the plan covers the shard's capacity, len_dev[b] += 1 after.
+// Fused append (medha_attn_decode_append / medha_kvp_decode_append / medha_decode_step_dev):
+// sequence b with app_mask[b] != 0 (app_mask == null: every sequence) appends row b of
+// k_app / v_app ([batch][h_kv][d] bf16) at local index len (len_dev mode: *len_dev) in the same
+// launch; the caller advances the host lengths after a successful call.
+struct DecodeAppend {
+  const void *k, *v;
+  const int32_t *mask;   // host [batch] or null
+};
+
 medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const void *q, int32_t h_q,
                                  const int64_t *q_pos, float scale, float *o, float *lse, void *ws,
                                  size_t ws_bytes, cudaStream_t st, const DecodeXchg *x = nullptr,
-                                 int64_t *len_dev = nullptr) {
+                                 int64_t *len_dev = nullptr, const DecodeAppend *app = nullptr) {
   if (batch < 0) return fail(MEDHA_EINVAL, "negative batch");
   if (batch == 0) return MEDHA_OK;
   if (!kvs || !q || !(q_pos || len_dev) || !o || !lse) return fail(MEDHA_EINVAL, "null argument");
@@ -228,6 +237,15 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
   if (ws_bytes < W.bytes) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, W.bytes);
 
   if (x && batch > kDecodeMaxSeqPerLaunch) return fail(MEDHA_ENOTSUP, "fused exchange needs batch <= 64");
+  if (app) {
+    if (!app->k || !app->v) return fail(MEDHA_EINVAL, "null k_new/v_new");
+    if (!aligned16(app->k) || !aligned16(app->v)) return fail(MEDHA_EINVAL, "k_new/v_new not 16-byte aligned");
+    if (!len_dev)
+      for (int b = 0; b < batch; ++b)
+        if ((!app->mask || app->mask[b]) && kvs[b].len + 1 > kvs[b].capacity)
+          return fail(MEDHA_ERANGE, "append at len %lld exceeds capacity %lld (sequence %d)", (long long)kvs[b].len,
+                      (long long)kvs[b].capacity, b);
+  }
   const int slots = 2 * num_sms();                 // two 4-warp CTAs per SM, persistent
   const int target = MEDHA_DEC_ITEMS * slots;       // work items per launch
   const int max_splits = std::min(kDecodeMaxSplits, kDecodeSplitW / G);
@@ -265,8 +283,9 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
     std::vector<int64_t> nvis(nb);
     for (int i = 0; i < nb; ++i) {
       const medha_kv_shard &kv = kvs[b0 + i];
+      const bool ap = app && (!app->mask || app->mask[b0 + i]);
       nvis[i] = len_dev ? kv.capacity
-                        : std::max<int64_t>(0, std::min<int64_t>(kv.len, q_pos[b0 + i] - kv.pos0 + 1));
+                        : std::max<int64_t>(0, std::min<int64_t>(kv.len + (ap ? 1 : 0), q_pos[b0 + i] - kv.pos0 + 1));
       total += nvis[i] * h_kv;
     }
     const int64_t per_cta =
@@ -289,6 +308,13 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
       S.len_dev = len_dev ? len_dev + b0 + i : nullptr;
       S.split_tokens = (int32_t)split_tokens;
       S.n_splits = (int32_t)ns;
+      S.cap = kv.capacity;
+      if (app && (!app->mask || app->mask[b0 + i])) {
+        const size_t row = (size_t)(b0 + i) * h_kv * d * 2;
+        S.k_app = reinterpret_cast<const uint4 *>(static_cast<const char *>(app->k) + row);
+        S.v_app = reinterpret_cast<const uint4 *>(static_cast<const char *>(app->v) + row);
+        S.t_app = kv.len;
+      }
       S.cta_begin = cta;
       S.slot_begin = cta;
       cta += (int)(ns * h_kv);
@@ -744,6 +770,19 @@ medha_status medha_attn_decode_partial(const medha_kv_shard *kvs_host, int32_t b
                              static_cast<cudaStream_t>(stream));
 }
 
+medha_status medha_attn_decode_append(medha_kv_shard *kvs_host, int32_t batch, const void *k_new, const void *v_new,
+                                      const int32_t *append_host, const void *q, int32_t h_q,
+                                      const int64_t *q_pos_host, float scale, float *o, float *lse, void *ws,
+                                      size_t ws_bytes, void *stream) {
+  DecodeAppend app{k_new, v_new, append_host};
+  medha_status s = decode_partial_impl(kvs_host, batch, q, h_q, q_pos_host, scale, o, lse, ws, ws_bytes,
+                                       static_cast<cudaStream_t>(stream), nullptr, nullptr, &app);
+  if (s == MEDHA_OK)
+    for (int b = 0; b < batch; ++b)
+      if (!append_host || append_host[b]) kvs_host[b].len += 1;
+  return s;
+}
+
 size_t medha_prefill_workspace_size(int64_t c, int32_t h_q, int32_t h_kv, int32_t d) {
   (void)h_kv;
   if (c <= 0 || h_q <= 0 || d <= 0) return 256;
@@ -921,9 +960,10 @@ size_t medha_kvp_workspace_size(int32_t world, int32_t batch, int32_t h_q, int32
   return kvp_buf_bytes(world, (int64_t)batch * h_q, d) + round_up(medha_decode_workspace_size(batch, h_q, h_kv, d), 256);
 }
 
-medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_host, int32_t batch, const void *q,
-                              int32_t h_q, const int64_t *q_pos_host, float scale, float *o_out, float *lse_out,
-                              void *o_out_bf16, void *ws, size_t ws_bytes, void *stream) {
+static medha_status kvp_decode_impl(medha_kvp_comm *comm, const medha_kv_shard *kvs_host, int32_t batch, const void *q,
+                                    int32_t h_q, const int64_t *q_pos_host, float scale, float *o_out, float *lse_out,
+                                    void *o_out_bf16, void *ws, size_t ws_bytes, void *stream,
+                                    const DecodeAppend *app) {
   if (!comm) return fail(MEDHA_EINVAL, "null comm");
   if (medha_status h = comm_health(comm)) return h;
   if (batch <= 0 || !kvs_host) return fail(MEDHA_EINVAL, "empty batch");
@@ -962,12 +1002,32 @@ medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_ho
     x.lse = lse_out;
     x.obf = static_cast<__nv_bfloat16 *>(o_out_bf16);
     return decode_partial_impl(kvs_host, batch, q, h_q, q_pos_host, scale, o_out, send + rows * d, dws,
-                               dws_bytes, st, &x);
+                               dws_bytes, st, &x, nullptr, app);
   }
   medha_status s = decode_partial_impl(kvs_host, batch, q, h_q, q_pos_host, scale, send, send + rows * d, dws,
-                                       dws_bytes, st);
+                                       dws_bytes, st, nullptr, nullptr, app);
   if (s) return s;
   return kvp_exchange_merge(comm, send, recv, rows, d, o_out, lse_out, o_out_bf16, st);
+}
+
+medha_status medha_kvp_decode(medha_kvp_comm *comm, const medha_kv_shard *kvs_host, int32_t batch, const void *q,
+                              int32_t h_q, const int64_t *q_pos_host, float scale, float *o_out, float *lse_out,
+                              void *o_out_bf16, void *ws, size_t ws_bytes, void *stream) {
+  return kvp_decode_impl(comm, kvs_host, batch, q, h_q, q_pos_host, scale, o_out, lse_out, o_out_bf16, ws, ws_bytes,
+                         stream, nullptr);
+}
+
+medha_status medha_kvp_decode_append(medha_kvp_comm *comm, medha_kv_shard *kvs_host, int32_t batch, const void *k_new,
+                                     const void *v_new, const int32_t *append_host, const void *q, int32_t h_q,
+                                     const int64_t *q_pos_host, float scale, float *o_out, float *lse_out,
+                                     void *o_out_bf16, void *ws, size_t ws_bytes, void *stream) {
+  DecodeAppend app{k_new, v_new, append_host};
+  medha_status s = kvp_decode_impl(comm, kvs_host, batch, q, h_q, q_pos_host, scale, o_out, lse_out, o_out_bf16, ws,
+                                   ws_bytes, stream, &app);
+  if (s == MEDHA_OK)
+    for (int b = 0; b < batch; ++b)
+      if (!append_host || append_host[b]) kvs_host[b].len += 1;
+  return s;
 }
 
 size_t medha_kvp_prefill_workspace_size(int32_t world, int64_t c, int32_t h_q, int32_t h_kv, int32_t d) {
@@ -1083,34 +1143,13 @@ medha_status medha_decode_step_dev(const medha_kv_shard *kvs_host, int32_t batch
                                    float *o, float *lse, void *ws, size_t ws_bytes, void *stream) {
   if (batch <= 0 || batch > kDecodeMaxSeqPerLaunch) return fail(MEDHA_ENOTSUP, "batch %d not in [1, 64]", batch);
   if (!kvs_host || !k_new || !v_new || !q || !len_dev || !o || !lse) return fail(MEDHA_EINVAL, "null argument");
-  if (!aligned16(k_new) || !aligned16(v_new) || (reinterpret_cast<uintptr_t>(len_dev) & 7))
-    return fail(MEDHA_EINVAL, "k_new/v_new not 16-byte aligned or len_dev not 8-byte aligned");
-  const int32_t h_kv = kvs_host[0].h_kv, d = kvs_host[0].d;
-  AppendDevParams ap;
-  memset(&ap, 0, sizeof(ap));
-  for (int b = 0; b < batch; ++b) {
-    const medha_kv_shard &kv = kvs_host[b];
-    medha_status s = check_shard(&kv);
-    if (s) return s;
-    if (kv.h_kv != h_kv || kv.d != d) return fail(MEDHA_ESHAPE, "shards disagree on h_kv/d");
-    ap.seq[b].k = static_cast<uint4 *>(kv.k);
-    ap.seq[b].v = static_cast<uint4 *>(kv.v);
-    ap.seq[b].hstride = head_stride(kv);
-    ap.seq[b].cap = kv.capacity;
-    ap.seq[b].pt = kv.page_table;
-    ap.seq[b].psl = kv.page_table ? log2_pow2(kv.page_size) : 0;
-  }
-  ap.k_new = static_cast<const uint4 *>(k_new);
-  ap.v_new = static_cast<const uint4 *>(v_new);
-  ap.len_dev = len_dev;
-  ap.batch = batch;
-  ap.h_kv = h_kv;
-  ap.vec_per_row = d / 8;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t total = (int64_t)batch * h_kv * (d / 8);
-  launch_pdl(kv_append_dev_kernel, dim3((unsigned)cdiv(total, 256)), dim3(256), 0, st, ap);
-  LAUNCH_CHECK("kv_append_dev_kernel");
-  return decode_partial_impl(kvs_host, batch, q, h_q, nullptr, scale, o, lse, ws, ws_bytes, st, nullptr, len_dev);
+  if (reinterpret_cast<uintptr_t>(len_dev) & 7) return fail(MEDHA_EINVAL, "len_dev not 8-byte aligned");
+  // ONE launch: the decode kernel's owner items store the new rows at *len_dev (dropped at or
+  // past the capacity), every item reads the new token from k_new / v_new, the last CTA out
+  // advances the lengths
+  DecodeAppend app{k_new, v_new, nullptr};
+  return decode_partial_impl(kvs_host, batch, q, h_q, nullptr, scale, o, lse, ws, ws_bytes,
+                             static_cast<cudaStream_t>(stream), nullptr, len_dev, &app);
 }
 
 #ifdef MEDHA_DECODE_TRACE

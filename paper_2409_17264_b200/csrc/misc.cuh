@@ -35,41 +35,6 @@ __global__ void kv_append_kernel(const uint4 *__restrict__ k_new, const uint4 *_
   }
 }
 
-// Device-length append (medha_decode_step_dev): token b's K/V rows ([batch][h_kv][D] 16-byte
-// vectors) go to local index len_dev[b] of shard b; the lengths are advanced by the decode.
-struct AppendDevSeq {
-  uint4 *k, *v;
-  int64_t hstride;
-  int64_t cap;            // capacity: appends at or past it are dropped (the host cannot check)
-  const int32_t *pt;
-  int32_t psl;
-};
-struct AppendDevParams {
-  const uint4 *k_new, *v_new;
-  const int64_t *len_dev;
-  int32_t batch, h_kv, vec_per_row;
-  AppendDevSeq seq[64];
-};
-__global__ void kv_append_dev_kernel(const __grid_constant__ AppendDevParams p) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const int64_t per_seq = (int64_t)p.h_kv * p.vec_per_row;
-  const int64_t total = per_seq * p.batch;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int b = (int)(i / per_seq);
-    const int64_t r = i - b * per_seq;
-    const int32_t h = (int32_t)(r / p.vec_per_row);
-    const int32_t e = (int32_t)(r - (int64_t)h * p.vec_per_row);
-    const AppendDevSeq &S = p.seq[b];
-    int64_t j = p.len_dev[b];
-    if (j < 0 || j >= S.cap) continue;
-    if (S.pt) j = ((int64_t)S.pt[j >> S.psl] << S.psl) | (j & ((1ll << S.psl) - 1));
-    const int64_t dst = ((int64_t)h * S.hstride + j) * p.vec_per_row + e;
-    S.k[dst] = p.k_new[i];
-    S.v[dst] = p.v_new[i];
-  }
-}
-
 // K5 ("combined using online-softmax"): part r starts at
 // parts + r*part_stride and holds o [rows][D] then lse [rows] (natural log);
 // part_stride = rows*(D+1) for the packed ABI layout (>= that for padded workspaces).  One warp per row; parts are
