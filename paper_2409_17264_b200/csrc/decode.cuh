@@ -91,6 +91,7 @@ struct DecodeSeq {
   const uint4 *v_app;
   int64_t t_app;
   int64_t cap;            // capacity (logical tokens) of the shard
+  int64_t safe_end;       // early start: tokens [0, safe_end) may be read before the grid dependency
   int32_t split_tokens;  // tokens per split, multiple of 64
   int32_t n_splits;      // splits per kv head
   int32_t cta_begin;     // first CTA of this sequence (CTAs ordered [kvh][split])
@@ -110,6 +111,7 @@ struct DecodeParams {
   int32_t n_seq;
   int32_t h_kv;
   int32_t h_q;
+  int32_t early;           // early start (see decode_splitkv_kernel); 0 in device-length mode
   // ---- fused KVP exchange over NVLink.  x_world == 0: off. ----
   // The last CTA of every (seq, kv head) pushes the unit's rank partial into every rank's
   // receive slot (peer memory mapped with CUDA IPC; at world 1 the local buffer), raises
@@ -169,11 +171,24 @@ struct __align__(16) DecodeSmem {
   uint32_t epoch;                // fused exchange: this call's epoch (kept out of registers)
 };
 
+// Grid dependency (PDL), once per thread: wait until the previous kernel on the stream has
+// completed and its writes are visible, then let the next kernel's CTAs start, and read the
+// fused exchange's epoch (written by the previous call's last CTA).
+template <int D, int G>
+__device__ __forceinline__ void grid_dep_sync(const DecodeParams &p, DecodeSmem<D, G> &sm, bool &waited) {
+  if (waited) return;
+  pdl_wait();
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) sm.epoch = (p.x_world > 0) ? *reinterpret_cast<volatile uint32_t *>(p.x_epoch) + 1u : 0u;
+  waited = true;
+}
+
 // One work item: split `split` of kv head `kvh` of sequence `sidx`.
 // kPaged: some sequence of the launch has a page table (a separate instantiation keeps the
 // contiguous path's register allocation untouched)
 template <int D, int G, bool kPaged>
-__device__ __forceinline__ void decode_item(const DecodeParams &p, const int item, DecodeSmem<D, G> &sm) {
+__device__ __forceinline__ void decode_item(const DecodeParams &p, const int item, DecodeSmem<D, G> &sm,
+                                            bool &waited) {
   constexpr int KCH = D / 32;   // 16-byte K chunks per lane per token
   constexpr int VCH = D / 64;   // 16-byte V chunks per lane per token
   constexpr int KS = D / 16;    // k-steps of the QK MMA
@@ -354,28 +369,35 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
     }
   };
 
-  // the owner of t_app (its split, or the last split when t_app lies past the visible keys)
-  // stores the new K / V rows of this kv head into the shard (never read back in this launch)
-  if (t_app >= 0 && split == (int)min64(t_app / S.split_tokens, S.n_splits - 1) && tid < 2 * (D / 8)) {
-    const int64_t row = tile_row(t_app & ~15ll) + (t_app & 15);
-    const int e = tid % (D / 8);
-    uint4 *dst = reinterpret_cast<uint4 *>(const_cast<__nv_bfloat16 *>(tid < D / 8 ? kbase : vbase) + row * D) + e;
-    *dst = (tid < D / 8 ? S.k_app : S.v_app)[(int64_t)kvh * (D / 8) + e];
-  }
   MEDHA_TRACE(0);
   constexpr int64_t kStep = 16 * kDecodeWarps;
   int64_t tb = t_begin + 16 * warp;
+  // early start: a tile reaching past safe_end (rows the previous kernel may still write)
+  // is loaded only after the grid dependency has resolved
+  const int64_t safe_end = S.safe_end;
+  auto gate = [&](int64_t t) {
+    if (!waited && t + 16 > safe_end) grid_dep_sync<D, G>(p, sm, waited);
+  };
 #if MEDHA_DEC_PINGPONG
   // 2x unrolled with ping-pong register buffers: tile i+1 loads while tile i computes,
   // without copying the prefetched fragments between iterations
   uint4 kb0[2][KCH], vb0[4][VCH], kb1[2][KCH], vb1[4][VCH];
-  if (tb < t_end) load_tile(tb, kb0, vb0);
+  if (tb < t_end) {
+    gate(tb);
+    load_tile(tb, kb0, vb0);
+  }
   while (tb < t_end) {
-    if (tb + kStep < t_end) load_tile(tb + kStep, kb1, vb1);
+    if (tb + kStep < t_end) {
+      gate(tb + kStep);
+      load_tile(tb + kStep, kb1, vb1);
+    }
     compute_tile(kb0, vb0, tb);
     tb += kStep;
     if (tb >= t_end) break;
-    if (tb + kStep < t_end) load_tile(tb + kStep, kb0, vb0);
+    if (tb + kStep < t_end) {
+      gate(tb + kStep);
+      load_tile(tb + kStep, kb0, vb0);
+    }
     compute_tile(kb1, vb1, tb);
     tb += kStep;
   }
@@ -401,6 +423,16 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
 #endif
 
   MEDHA_TRACE(1);
+  // every global write below follows the grid dependency
+  grid_dep_sync<D, G>(p, sm, waited);
+  // the owner of t_app (its split, or the last split when t_app lies past the visible keys)
+  // stores the new K / V rows of this kv head into the shard (never read back in this launch)
+  if (t_app >= 0 && split == (int)min64(t_app / S.split_tokens, S.n_splits - 1) && tid < 2 * (D / 8)) {
+    const int64_t row = tile_row(t_app & ~15ll) + (t_app & 15);
+    const int e = tid % (D / 8);
+    uint4 *dst = reinterpret_cast<uint4 *>(const_cast<__nv_bfloat16 *>(tid < D / 8 ? kbase : vbase) + row * D) + e;
+    *dst = (tid < D / 8 ? S.k_app : S.v_app)[(int64_t)kvh * (D / 8) + e];
+  }
   // ---- per-warp reduction of l over the 4 lanes of a row, publish to smem --------------
   l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
   l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
@@ -641,29 +673,40 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_splitkv_kernel(const
 #ifdef MEDHA_DECODE_TRACE
   const unsigned long long t_entry = gtimer();
 #endif
-  // PDL: this grid's CTAs may be resident before the previous kernel on the stream ends;
-  // nothing is read or written before it has (KV rows, queue counters, outputs)
-  pdl_wait();
-  pdl_launch_dependents();
-  // fused exchange: this call's epoch = the last completed call's + 1 (same on every rank:
-  // each rank's word advances once per call of the collective)
-  if (threadIdx.x == 0) sm.epoch = (p.x_world > 0) ? *reinterpret_cast<volatile uint32_t *>(p.x_epoch) + 1u : 0u;
+  // PDL: this grid's CTAs may be resident before the previous kernel on the stream ends.
+  // Early start (p.early, host-length mode): CTA b runs its first item (b) right away and
+  // streams the K/V rows below the item's safe_end before the grid dependency resolves.
+  // Why that is safe: every kernel of this library triggers its dependents only after its
+  // own griddepcontrol.wait (kv_append_kernel only at exit), so when this grid starts, every
+  // kernel before the immediately preceding one has completed; the preceding one - if it is
+  // a decode of this library - writes at most its appended row (index len - 1 of ours),
+  // which is at or past safe_end = len - 1; the query is only written by foreign kernels
+  // (which trigger at exit) or by kv_append_kernel.  Every global WRITE (partials, counters,
+  // outputs, the appended rows, the exchange) and every read of a counter, length or epoch
+  // comes after grid_dep_sync.  Otherwise (and in device-length mode) the CTA waits first.
+  bool waited = false;
+  if (!p.early) grid_dep_sync<D, G>(p, sm, waited);
 #ifdef MEDHA_DECODE_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     g_ltrace[g_ltrace_n & 63][0] = t_entry;
     g_ltrace[g_ltrace_n & 63][1] = gtimer();
   }
 #endif
-  // persistent: take work items from the queue until it runs dry
-  for (;;) {
-    if (threadIdx.x == 0) sm.item = (int)atomicAdd(p.work, 1u);
-    __syncthreads();
-    const int item = sm.item;
+  // persistent: the first item is this CTA's own (grid <= items), the rest come from the
+  // queue (claimed after the grid dependency: the previous launch's last CTA resets it)
+  for (int first = 1;; first = 0) {
+    if (!first) {
+      if (threadIdx.x == 0) sm.item = (int)gridDim.x + (int)atomicAdd(p.work, 1u);
+      __syncthreads();
+    }
+    const int item = first ? (int)blockIdx.x : sm.item;
     __syncthreads();
     if (item >= p.n_items) break;
-    decode_item<D, G, kPaged>(p, item, sm);
+    decode_item<D, G, kPaged>(p, item, sm, waited);
     __syncthreads();
   }
+  grid_dep_sync<D, G>(p, sm, waited);
+  __syncthreads();
   // fused KVP exchange: units are merged after this CTA's items (no CTA ever spins while
   // this rank still has unprocessed items, so the wait cannot deadlock)
   if (p.x_world > 0)

@@ -264,6 +264,8 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
     p.n_seq = nb;
     p.h_kv = h_kv;
     p.h_q = h_q;
+    static const bool early_ok = getenv_flag("MEDHA_DEC_EARLY", 1) != 0;
+    p.early = (early_ok && !len_dev) ? 1 : 0;
     if (x) {
       p.x_world = x->world;
       p.x_rank = x->rank;
@@ -309,6 +311,7 @@ medha_status decode_partial_impl(const medha_kv_shard *kvs, int32_t batch, const
       S.split_tokens = (int32_t)split_tokens;
       S.n_splits = (int32_t)ns;
       S.cap = kv.capacity;
+      S.safe_end = len_dev ? 0 : std::max<int64_t>(0, kv.len - 1);
       if (app && (!app->mask || app->mask[b0 + i])) {
         const size_t row = (size_t)(b0 + i) * h_kv * d * 2;
         S.k_app = reinterpret_cast<const uint4 *>(static_cast<const char *>(app->k) + row);

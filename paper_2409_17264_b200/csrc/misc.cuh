@@ -14,8 +14,9 @@ __global__ void kv_append_kernel(const uint4 *__restrict__ k_new, const uint4 *_
                                  int32_t vec_per_row, int64_t hstride, int64_t len,
                                  const int32_t *__restrict__ pt, int32_t psl,
                                  const uint4 *__restrict__ cp_src, uint4 *__restrict__ cp_dst, int64_t cp_n) {
+  // no early trigger: a following decode may read K/V rows (and the staged query) before its
+  // own grid dependency resolves, so it must not start while this kernel writes them
   pdl_wait();
-  pdl_launch_dependents();
 #ifdef MEDHA_DECODE_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0) g_ltrace[g_ltrace_n & 63][3] = gtimer();
 #endif

@@ -33,6 +33,18 @@ for n in (1 << 20, 1 << 17):
             sh.len = L
             M.attn_decode_append([sh], k_new, v_new, q, [n - 1], o=o, lse=lse, ws=ws)
         arms["fused"] = fused
+
+        def fused_noapp():        # same call, append flag off (no owner write, no redirect)
+            sh.len = L + 1
+            M.attn_decode_append([sh], k_new, v_new, q, [n - 1], append=[False], o=o, lse=lse, ws=ws)
+        arms["fused_noapp"] = fused_noapp
+
+        def partial_lenreset():   # plain decode with the host length rewritten every step
+            sh.len = L + 1
+            M.attn_decode_partial([sh], q, [n - 1], o=o, lse=lse, ws=ws)
+        arms["partial_lenreset"] = partial_lenreset
+    if os.environ.get("AB_REVERSE") == "1":
+        arms = dict(reversed(list(arms.items())))
     res = {}
     for rep in range(3):
         for name, fn in arms.items():

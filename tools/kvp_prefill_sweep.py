@@ -1,8 +1,8 @@
 """Chunk x KVP sweep of chunked-prefill attention at 2M-10M prefixes (the
 analogue of the paper's fig:kvpscaling:prefill:ttft, Eq. 6).
 
-    python scripts/kvp_prefill_sweep.py                     (KVP = 1)
-    torchrun --nproc-per-node P scripts/kvp_prefill_sweep.py (KVP = P)
+    python tools/kvp_prefill_sweep.py                     (KVP = 1)
+    torchrun --nproc-per-node P tools/kvp_prefill_sweep.py (KVP = P)
 
 Llama-3 8B layer shape.  Every rank holds an equal slice of the prefix; the tail rank also
 holds the chunk's own K/V.  A step = the KVP prefill of one chunk (local tcgen05 partial +

@@ -1,5 +1,5 @@
 """Prefill-chunk TFLOP/s sweep (configs[2]) using bench.py's measurement code.
-    python scripts/prefill_sweep.py [prefixes] [chunks] [label]
+    python tools/prefill_sweep.py [prefixes] [chunks] [label]
 MEDHA_LIB_PATH selects an experiment variant of the library (same-box A/B)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
