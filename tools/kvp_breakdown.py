@@ -1,7 +1,8 @@
 """Experiment (torchrun): where the multi-GPU KVP decode step spends the time beyond the
 per-rank decode kernel.  Every variant runs 30 back-to-back steps (CUDA events, max over
 ranks): the rank-local decode alone, + kv_append on the tail rank, the fused-exchange
-KVP decode with and without the append, and the NCCL all-gather path."""
+KVP decode with and without the append (two launches, or one with medha_kvp_decode_append),
+and the NCCL all-gather path.  KVP_TOKENS sets the global KV length (default 2^20)."""
 import json
 import os
 import sys
@@ -58,6 +59,13 @@ def fused_append():
     fused()
 
 
+def fused_append_one_launch():
+    # the tail rank's append rides in the decode launch (medha_kvp_decode_append)
+    if tail:
+        sh.len = len_before
+    M.kvp_decode_append(comm, [sh], k_new, v_new, q, [N - 1], append=[tail], ws=kws, o=o, lse=lse)
+
+
 def nccl():
     M.attn_decode_partial([sh], q, [N - 1], o=parts[:H_Q * D].view(1, H_Q, D), lse=parts[H_Q * D:].view(1, H_Q), ws=dws)
     M.kvp_exchange_merge(comm, parts, H_Q, D, o, lse, ws=xws)
@@ -82,7 +90,8 @@ def timed(fn, iters=30, warm=5):
 
 
 res = {"world": world, "tokens": N}
-for name, fn in (("local", local), ("local+append", local_append), ("fused", fused), ("fused+append", fused_append)):
+for name, fn in (("local", local), ("local+append", local_append), ("fused", fused), ("fused+append", fused_append),
+                 ("fused_append_1launch", fused_append_one_launch)):
     res[name] = timed(fn)
 comm.set_p2p(False)
 res["nccl"] = timed(nccl)
