@@ -249,10 +249,14 @@ def bench_decode(args, rank, world, M):
     l_h = torch.empty((H_Q,), dtype=torch.float32).pin_memory()
     sws = M.decode_step_workspace(world, H_Q, H_KV, D)
 
+    # the serving loop's prepared step (medha_decode_plan: host buffers, comm and workspace
+    # resolved once; each step = the H2D-reading staging launch + the decode launch)
+    plan = M.DecodePlan(comm, sh, q_h, k_h if tail else None, v_h if tail else None, o_h, l_h, sws)
+
     def e2e_step():
         if tail:
             sh.len = len_before
-        M.decode_step_host(comm, sh, tail, q_h, k_h if tail else None, v_h if tail else None, new_pos, o_h, l_h, sws)
+        plan.step(sh, tail, new_pos, stream)
         stream.synchronize()   # the host reads the step's result
 
     for _ in range(args.warmup):
@@ -271,6 +275,7 @@ def bench_decode(args, rank, world, M):
     e2e_ms = _max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     # parity of the e2e output against the device path (same inputs)
     e2e_diff = float((o_h - o_out[0].cpu()).abs().max())
+    plan.close()
 
     bytes_total = acc.decode_bytes(N_KV, H_KV, D)              # all ranks together
     bytes_rank = acc.decode_bytes(sh.len, H_KV, D)
@@ -402,6 +407,97 @@ def bench_70b_decode(M, iters=5, warm=2):
         del sh
         torch.cuda.empty_cache()
     return res
+
+
+def mixed_two_streams(M, shorts, qd, qpos_d, sh_long, q_long, p0_long, iters=5, warm=2):
+    """SURVEY N2 / P:89, P:752 (prefill and decode batched together): a batch of decodes
+    (one decode launch over all `shorts`) beside one prefill chunk, run (a) one after the
+    other on one stream and (b) concurrently on two streams (the prefill's 1-CTA-per-SM grid
+    and the decode's 2-CTA-per-SM grid then share the SMs as the block scheduler places
+    them).  Returns per-step ms of both arms and the max |difference| of their outputs
+    (same kernels and split plans: 0 expected)."""
+    import torch
+    B = len(shorts)
+    c = q_long.shape[0]
+    od = [torch.empty((B, H_Q, D), device="cuda") for _ in range(2)]
+    ld = [torch.empty((B, H_Q), device="cuda") for _ in range(2)]
+    op = [torch.empty((c, H_Q, D), device="cuda") for _ in range(2)]
+    lp = [torch.empty((c, H_Q), device="cuda") for _ in range(2)]
+    s_main = torch.cuda.current_stream()
+    s_dec = torch.cuda.Stream()
+    dws = [torch.zeros(M.lib.medha_decode_workspace_size(B, H_Q, H_KV, D), dtype=torch.uint8, device="cuda")
+           for _ in range(2)]
+    pws = [torch.zeros(M.lib.medha_prefill_workspace_size(c, H_Q, H_KV, D), dtype=torch.uint8, device="cuda")
+           for _ in range(2)]
+
+    def serial(k):
+        M.attn_prefill_chunk(sh_long, q_long, p0_long, o=op[k], lse=lp[k], ws=pws[k])
+        M.attn_decode_partial(shorts, qd, qpos_d, o=od[k], lse=ld[k], ws=dws[k])
+
+    def concurrent(k):
+        s_dec.wait_stream(s_main)
+        M.attn_prefill_chunk(sh_long, q_long, p0_long, o=op[k], lse=lp[k], ws=pws[k])
+        with torch.cuda.stream(s_dec):
+            M.attn_decode_partial(shorts, qd, qpos_d, o=od[k], lse=ld[k], ws=dws[k], stream=s_dec)
+        s_main.wait_stream(s_dec)
+
+    res = {}
+    for name, fn, k in (("one_stream", serial, 0), ("two_streams", concurrent, 1), ("one_stream_again", serial, 0)):
+        for _ in range(warm):
+            fn(k)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s_main)
+        for _ in range(iters):
+            fn(k)
+        e1.record(s_main)
+        torch.cuda.synchronize()
+        res[name] = e0.elapsed_time(e1) / iters
+    # the arms alone, for the sum / max bounds
+    for name, fn in (("prefill_alone", lambda: M.attn_prefill_chunk(sh_long, q_long, p0_long, o=op[0], lse=lp[0],
+                                                                     ws=pws[0])),
+                     ("decodes_alone", lambda: M.attn_decode_partial(shorts, qd, qpos_d, o=od[0], lse=ld[0],
+                                                                     ws=dws[0]))):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        res[name] = e0.elapsed_time(e1) / iters
+    serial(0)
+    concurrent(1)
+    torch.cuda.synchronize()
+    diff = max(float((od[0] - od[1]).abs().max()), float((op[0] - op[1]).abs().max()))
+    return res, diff, (od[1], ld[1], op[1], lp[1])
+
+
+def bench_mixed_n2(M, iters=5, warm=2):
+    """SURVEY N2 at a size where the decodes are not negligible: 32 decodes over 64K-token
+    KVs (8 GiB of K/V) beside one c = 128 chunk at a 2M prefix (4.4 TFLOP), 8B shape, one GPU."""
+    import torch
+    import synth
+    from paper_2409_17264_b200 import accounting as acc
+    B, n_dec, c, P0 = 32, 1 << 16, 128, 1 << 21
+    shorts = [build_range(M, 0, n_dec, H_KV, D, seed=SEED + 200 + i) for i in range(B)]
+    qd = synth.queries(SEED + 201, B, H_Q, D, device="cuda", amp=4.0)
+    sh_long = build_range(M, 0, P0 + c, H_KV, D, seed=SEED + 202)
+    q_long = synth.queries(SEED + 203, c, H_Q, D, device="cuda", amp=1.0, t0=P0)
+    t, diff, _ = mixed_two_streams(M, shorts, qd, [n_dec - 1] * B, sh_long, q_long, P0, iters, warm)
+    fl = acc.prefill_chunk_flops(c, P0, H_Q, D)
+    by = acc.decode_bytes(B * n_dec, H_KV, D)
+    out = {"workload": f"{B} x {n_dec}-token decodes + one c={c} chunk at a {P0}-token prefix (8B shape, N=1)",
+           "decode_bytes": by, "chunk_tflop": round(fl / 1e12, 3),
+           "ms": {k: round(v, 4) for k, v in t.items()},
+           "two_stream_speedup": round(min(t["one_stream"], t["one_stream_again"]) / t["two_streams"], 4),
+           "max_abs_diff_between_arms": diff,
+           "note": "parity of both arms vs the fp64 oracle: tests/test_gpu_mixed.py (same code path, smaller sizes)"}
+    del shorts, sh_long
+    torch.cuda.empty_cache()
+    return out
 
 
 def bench_mixed(M, rank, world, iters=5, warm=3):
@@ -607,6 +703,7 @@ def main():
         torch.cuda.empty_cache()
         extra["decode_70b_10M"] = bench_70b_decode(M)
         extra["decode_cuda_graph"] = bench_graph_decode(M)
+        extra["mixed_n2"] = bench_mixed_n2(M)
     if world in (1, 4) and not args.no_extra:
         mixed = bench_mixed(M, rank, world)
         if rank == 0:
@@ -630,7 +727,7 @@ def main():
                          "kernel_timing": f"CUDA events around 1 in {r['ev_every']} decode launches of the timed region"},
             "e2e": {"value": round(r["bytes_total"] / (r["e2e_ms"] * 1e-3) / 1e9, 1), "unit": "GB/s",
                     "ms_per_step": round(r["e2e_ms"], 5), "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
-                    "api": "medha_decode_step_host", "max_abs_vs_device_path": r["e2e_diff"]},
+                    "api": "medha_decode_plan_step (prepared medha_decode_step_host)", "max_abs_vs_device_path": r["e2e_diff"]},
             "gpu_launches": r["launches"],
             "kvp_exchange": r["exchange"],
             "clocks": r["clocks"],

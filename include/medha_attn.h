@@ -311,6 +311,25 @@ medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, in
                                     void *ws, size_t ws_bytes, void *stream);
 
 /*
+ * decode plan (the per-layer object of a serving loop around medha_decode_step_host): fixes
+ * the communicator (or NULL), the shard geometry (h_kv, d of `kv`), h_q, scale, the host
+ * buffers and the workspace once - their validation, mapped-pointer lookups
+ * (cudaPointerGetAttributes) and workspace carving happen in medha_decode_plan_create - so
+ * each medha_decode_plan_step(plan, kv, append, q_pos, stream) only validates the shard and
+ * launches (same work and semantics as medha_decode_step_host with those arguments; k_new /
+ * v_new may be NULL in the plan when no step appends).  The plan holds no device memory;
+ * the buffers it names must outlive it.  Not thread-safe per plan.
+ */
+typedef struct medha_decode_plan medha_decode_plan;
+medha_status medha_decode_plan_create(medha_kvp_comm *comm, const medha_kv_shard *kv, int32_t h_q,
+                                      float scale, const void *q_host, const void *k_new_host,
+                                      const void *v_new_host, float *o_host, float *lse_host,
+                                      void *ws, size_t ws_bytes, medha_decode_plan **out);
+medha_status medha_decode_plan_step(medha_decode_plan *plan, medha_kv_shard *kv, int32_t append,
+                                    int64_t q_pos, void *stream);
+medha_status medha_decode_plan_destroy(medha_decode_plan *plan);
+
+/*
  * decode_step_dev (device-side lengths, CUDA-graph-capturable; P:178-183
  * decode scans the whole KV, P:597-599 per-shard partial).  One decode token for each of
  * `batch` (1..64) sequences on this GPU, all lengths on the DEVICE:

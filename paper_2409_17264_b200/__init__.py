@@ -20,7 +20,7 @@ from typing import List, Optional, Sequence
 import torch
 
 __all__ = ["lib", "MedhaError", "KVShard", "kv_append", "attn_decode_partial", "attn_decode_append",
-           "kvp_decode_append", "attn_prefill_chunk",
+           "kvp_decode_append", "attn_prefill_chunk", "DecodePlan",
            "merge_partials", "KVPComm", "kvp_decode", "kvp_exchange_merge", "exchange_workspace", "kvp_prefill_chunk", "decode_step_host",
            "hbm_read_probe", "decode_workspace", "prefill_workspace", "kvp_workspace", "LIB_PATH"]
 
@@ -487,6 +487,53 @@ def decode_step_host(comm: Optional[KVPComm], shard: KVShard, append: bool, q_ho
                                       _ptr(o_host), _ptr(lse_host), _ptr(ws), ws.numel(), _stream(stream)),
            "decode_step_host")
     shard.len = sh.len
+
+
+_sig("medha_decode_plan_create", _i32, _vp, _P(_Shard), _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(_vp))
+_sig("medha_decode_plan_step", _i32, _vp, _P(_Shard), _i32, _i64, _vp)
+_sig("medha_decode_plan_destroy", _i32, _vp)
+
+
+class DecodePlan:
+    """Prepared decode_step_host (include/medha_attn.h `medha_decode_plan_*`): the host
+    buffers, communicator, shard geometry and workspace are resolved once; each step() is
+    one C call that launches the step (no per-step pointer queries or argument re-checks
+    beyond the shard).  The tensors passed here must stay alive with the plan; step() takes
+    the same shard (its len advances) every time."""
+
+    def __init__(self, comm: Optional["KVPComm"], shard: KVShard, q_host: torch.Tensor,
+                 k_host: Optional[torch.Tensor], v_host: Optional[torch.Tensor], o_host: torch.Tensor,
+                 lse_host: Optional[torch.Tensor], ws: torch.Tensor, scale=None):
+        h_q, d = q_host.shape
+        self._keep = (comm, q_host, k_host, v_host, o_host, lse_host, ws)
+        self._sh = shard.c()
+        h = ctypes.c_void_p()
+        _check(lib.medha_decode_plan_create(comm.handle if comm is not None else None, ctypes.byref(self._sh), h_q,
+                                            _scale(scale, d), _ptr(q_host), _ptr(k_host), _ptr(v_host), _ptr(o_host),
+                                            _ptr(lse_host), _ptr(ws), ws.numel(), ctypes.byref(h)), "decode_plan_create")
+        self.handle = h
+        self._step = lib.medha_decode_plan_step
+        self._shref = ctypes.byref(self._sh)
+
+    def step(self, shard: KVShard, append: bool, q_pos: int, stream=None) -> None:
+        """One decode step (async on the stream; outputs valid after it is synchronised)."""
+        sh = self._sh                # the plan's shard struct: same k / v / capacity / pos0
+        sh.len = shard.len
+        rc = self._step(self.handle, self._shref, 1 if append else 0, q_pos, _stream(stream))
+        if rc:
+            raise MedhaError(rc, "decode_plan_step")
+        shard.len = sh.len
+
+    def close(self):
+        if self.handle:
+            lib.medha_decode_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def decode_step_workspace(world, h_q, h_kv, d, device=None, stream=None):

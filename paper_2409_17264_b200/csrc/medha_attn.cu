@@ -1073,71 +1073,154 @@ size_t medha_decode_step_workspace_size(int32_t world, int32_t h_q, int32_t h_kv
   return stage + inner;
 }
 
-medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, int32_t append, const void *q_host,
-                                    const void *k_new_host, const void *v_new_host, int32_t h_q, int64_t q_pos,
-                                    float scale, float *o_host, float *lse_host, void *ws, size_t ws_bytes,
-                                    void *stream) {
+}  // extern "C"
+
+namespace {
+// decode_step_host, split into the per-call-invariant part (validation of the host buffers,
+// their mapped device views, workspace carving: StepSetup) and the per-step launches
+// (step_run).  medha_decode_plan keeps a StepSetup across steps.
+struct StepSetup {
+  medha_kvp_comm *comm;
+  int32_t h_q, h_kv, d;
+  float scale;
+  const void *q_host, *k_host, *v_host;
+  float *o_host, *lse_host;
+  char *inner;
+  size_t inner_bytes;
+  void *q_dev, *k_dev, *v_dev;
+  float *o_dev, *lse_dev;
+  const void *q_map, *k_map, *v_map;
+  float *o_map, *l_map;
+  bool zc_in_q, zc_in_kv, zc_out;
+};
+
+medha_status step_setup(medha_kvp_comm *comm, const medha_kv_shard *kv, int32_t h_q, float scale, const void *q_host,
+                        const void *k_new_host, const void *v_new_host, float *o_host, float *lse_host, void *ws,
+                        size_t ws_bytes, StepSetup *S) {
   medha_status s = check_shard(kv);
   if (s) return s;
   if (!q_host || !o_host) return fail(MEDHA_EINVAL, "null host buffer");
-  if (append && (!k_new_host || !v_new_host)) return fail(MEDHA_EINVAL, "null k/v host buffer");
   const int32_t d = kv->d, h_kv = kv->h_kv;
   const int32_t world = comm ? comm->world : 1;
   const size_t need = medha_decode_step_workspace_size(world, h_q, h_kv, d);
   if (!ws || ws_bytes < need) return fail(MEDHA_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  memset(S, 0, sizeof(*S));
+  S->comm = comm;
+  S->h_q = h_q;
+  S->h_kv = h_kv;
+  S->d = d;
+  S->scale = scale;
+  S->q_host = q_host;
+  S->k_host = k_new_host;
+  S->v_host = v_new_host;
+  S->o_host = o_host;
+  S->lse_host = lse_host;
   // the inner (decode / KVP) workspace first: its counter block stays at offset 0 for any
   // shape; the staging buffers follow it
-  const size_t inner_bytes = round_up(medha_kvp_workspace_size(std::max(world, 1), 1, h_q, h_kv, d), 256);
-  char *inner = static_cast<char *>(ws);
-  char *b = inner + inner_bytes;
+  S->inner_bytes = round_up(medha_kvp_workspace_size(std::max(world, 1), 1, h_q, h_kv, d), 256);
+  S->inner = static_cast<char *>(ws);
+  char *b = S->inner + S->inner_bytes;
   const size_t qb = (size_t)h_q * d * 2, kb = (size_t)h_kv * d * 2;
-  void *q_dev = b;
+  S->q_dev = b;
   b += round_up(qb, 256);
-  void *k_dev = b;
+  S->k_dev = b;
   b += round_up(kb, 256);
-  void *v_dev = b;
+  S->v_dev = b;
   b += round_up(kb, 256);
-  float *o_dev = reinterpret_cast<float *>(b);
+  S->o_dev = reinterpret_cast<float *>(b);
   b += round_up((size_t)h_q * d * 4, 256);
-  float *lse_dev = reinterpret_cast<float *>(b);
-  b += round_up((size_t)h_q * 4, 256);
+  S->lse_dev = reinterpret_cast<float *>(b);
+  // mapped (zero-copy) device views of the host buffers
+  S->q_map = mapped_host_view(q_host);
+  S->k_map = k_new_host ? mapped_host_view(k_new_host) : nullptr;
+  S->v_map = v_new_host ? mapped_host_view(v_new_host) : nullptr;
+  S->zc_in_q = S->q_map && aligned16(S->q_map) && (qb % 16 == 0);
+  S->zc_in_kv = S->k_map && S->v_map && aligned16(S->k_map) && aligned16(S->v_map);
+  S->o_map = static_cast<float *>(mapped_host_view(o_host));
+  S->l_map = lse_host ? static_cast<float *>(mapped_host_view(lse_host)) : nullptr;
+  S->zc_out = S->o_map && aligned16(S->o_map) && (!lse_host || S->l_map);
+  return MEDHA_OK;
+}
+
+medha_status step_run(const StepSetup &S, medha_kv_shard *kv, int32_t append, int64_t q_pos, cudaStream_t st) {
+  medha_status s;
+  if (append && (!S.k_host || !S.v_host)) return fail(MEDHA_EINVAL, "null k/v host buffer");
+  if (kv->h_kv != S.h_kv || kv->d != S.d) return fail(MEDHA_ESHAPE, "shard does not match the step setup");
+  const size_t qb = (size_t)S.h_q * S.d * 2, kb = (size_t)S.h_kv * S.d * 2;
   // Inputs: with mapped pinned host buffers, ONE launch reads q, k_new and v_new over the
-  // host link (q into the workspace, K/V appended straight into the shard); otherwise three
+  // host link (q into the workspace, K/V appended straight into the shard); otherwise
   // cudaMemcpyAsync + kv_append.
-  const void *q_map = mapped_host_view(q_host);
-  const void *k_map = append ? mapped_host_view(k_new_host) : nullptr;
-  const void *v_map = append ? mapped_host_view(v_new_host) : nullptr;
-  const bool zc_in = q_map && aligned16(q_map) && (qb % 16 == 0) &&
-                     (!append || (k_map && v_map && aligned16(k_map) && aligned16(v_map)));
-  if (zc_in) {
+  if (S.zc_in_q && (!append || S.zc_in_kv)) {
+    if ((s = check_shard(kv))) return s;
     if (append && kv->len + 1 > kv->capacity) return fail(MEDHA_ERANGE, "append exceeds capacity");
-    if ((s = kv_append_impl(kv, k_map, v_map, append ? 1 : 0, q_map, q_dev, (int64_t)qb, st))) return s;
+    if ((s = kv_append_impl(kv, S.k_map, S.v_map, append ? 1 : 0, S.q_map, S.q_dev, (int64_t)qb, st))) return s;
   } else {
-    CUDA_TRY(cudaMemcpyAsync(q_dev, q_host, qb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(S.q_dev, S.q_host, qb, cudaMemcpyHostToDevice, st));
     if (append) {
-      CUDA_TRY(cudaMemcpyAsync(k_dev, k_new_host, kb, cudaMemcpyHostToDevice, st));
-      CUDA_TRY(cudaMemcpyAsync(v_dev, v_new_host, kb, cudaMemcpyHostToDevice, st));
-      if ((s = medha_kv_append(kv, k_dev, v_dev, 1, stream))) return s;
+      CUDA_TRY(cudaMemcpyAsync(S.k_dev, S.k_host, kb, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(S.v_dev, S.v_host, kb, cudaMemcpyHostToDevice, st));
+      if ((s = medha_kv_append(kv, S.k_dev, S.v_dev, 1, st))) return s;
     }
   }
   // Outputs: written by the decode kernel straight into mapped pinned host buffers
   // (visible to the host once the stream is synchronised), else staged and copied back.
-  float *o_map = static_cast<float *>(mapped_host_view(o_host));
-  float *l_map = lse_host ? static_cast<float *>(mapped_host_view(lse_host)) : nullptr;
-  const bool zc_out = o_map && aligned16(o_map) && (!lse_host || l_map);
-  float *o_tgt = zc_out ? o_map : o_dev;
-  float *l_tgt = zc_out ? (lse_host ? l_map : lse_dev) : lse_dev;
+  float *o_tgt = S.zc_out ? S.o_map : S.o_dev;
+  float *l_tgt = S.zc_out ? (S.lse_host ? S.l_map : S.lse_dev) : S.lse_dev;
   const int64_t qp = q_pos;
-  if (comm)
-    s = medha_kvp_decode(comm, kv, 1, q_dev, h_q, &qp, scale, o_tgt, l_tgt, nullptr, inner, inner_bytes, stream);
+  if (S.comm)
+    s = medha_kvp_decode(S.comm, kv, 1, S.q_dev, S.h_q, &qp, S.scale, o_tgt, l_tgt, nullptr, S.inner, S.inner_bytes, st);
   else
-    s = decode_partial_impl(kv, 1, q_dev, h_q, &qp, scale, o_tgt, l_tgt, inner, inner_bytes, st);
+    s = decode_partial_impl(kv, 1, S.q_dev, S.h_q, &qp, S.scale, o_tgt, l_tgt, S.inner, S.inner_bytes, st);
   if (s) return s;
-  if (!zc_out) {
-    CUDA_TRY(cudaMemcpyAsync(o_host, o_dev, (size_t)h_q * d * 4, cudaMemcpyDeviceToHost, st));
-    if (lse_host) CUDA_TRY(cudaMemcpyAsync(lse_host, lse_dev, (size_t)h_q * 4, cudaMemcpyDeviceToHost, st));
+  if (!S.zc_out) {
+    CUDA_TRY(cudaMemcpyAsync(S.o_host, S.o_dev, (size_t)S.h_q * S.d * 4, cudaMemcpyDeviceToHost, st));
+    if (S.lse_host) CUDA_TRY(cudaMemcpyAsync(S.lse_host, S.lse_dev, (size_t)S.h_q * 4, cudaMemcpyDeviceToHost, st));
   }
+  return MEDHA_OK;
+}
+}  // namespace
+
+struct medha_decode_plan {
+  StepSetup setup;
+};
+
+extern "C" {
+
+medha_status medha_decode_step_host(medha_kvp_comm *comm, medha_kv_shard *kv, int32_t append, const void *q_host,
+                                    const void *k_new_host, const void *v_new_host, int32_t h_q, int64_t q_pos,
+                                    float scale, float *o_host, float *lse_host, void *ws, size_t ws_bytes,
+                                    void *stream) {
+  StepSetup S;
+  medha_status s = step_setup(comm, kv, h_q, scale, q_host, append ? k_new_host : nullptr,
+                              append ? v_new_host : nullptr, o_host, lse_host, ws, ws_bytes, &S);
+  if (s) return s;
+  return step_run(S, kv, append, q_pos, static_cast<cudaStream_t>(stream));
+}
+
+medha_status medha_decode_plan_create(medha_kvp_comm *comm, const medha_kv_shard *kv, int32_t h_q, float scale,
+                                      const void *q_host, const void *k_new_host, const void *v_new_host,
+                                      float *o_host, float *lse_host, void *ws, size_t ws_bytes,
+                                      medha_decode_plan **out) {
+  if (!out) return fail(MEDHA_EINVAL, "null plan pointer");
+  medha_decode_plan *p = new medha_decode_plan();
+  medha_status s = step_setup(comm, kv, h_q, scale, q_host, k_new_host, v_new_host, o_host, lse_host, ws, ws_bytes,
+                              &p->setup);
+  if (s) {
+    delete p;
+    return s;
+  }
+  *out = p;
+  return MEDHA_OK;
+}
+
+medha_status medha_decode_plan_step(medha_decode_plan *plan, medha_kv_shard *kv, int32_t append, int64_t q_pos,
+                                    void *stream) {
+  if (!plan || !kv) return fail(MEDHA_EINVAL, "null argument");
+  return step_run(plan->setup, kv, append, q_pos, static_cast<cudaStream_t>(stream));
+}
+
+medha_status medha_decode_plan_destroy(medha_decode_plan *plan) {
+  delete plan;
   return MEDHA_OK;
 }
 

@@ -343,3 +343,43 @@ def test_kvp_workspace_reused_across_shapes(M, comm, fused):
             assert torch.equal(o, o1) and torch.equal(lse, l1), f"shape {i}"
     finally:
         comm.set_p2p(True)
+
+
+@pytest.mark.parametrize("use_comm,pinned", [(False, True), (True, True), (False, False)])
+def test_decode_plan_equals_decode_step_host(M, comm, use_comm, pinned):
+    """medha_decode_plan_step (prepared host buffers / workspace) = medha_decode_step_host,
+    step after step; pinned (zero-copy) and pageable (staged copies) host buffers."""
+    h_kv, G, d, N, steps = 8, 4, 128, 30000, 3
+    k, v = make_global_kv(700, N + steps, h_kv, d)
+    qs = synth.queries(701, steps, h_kv * G, d, amp=6.0)
+    pin = (lambda t: t.pin_memory()) if pinned else (lambda t: t)
+    c = comm if use_comm else None
+    res = []
+    for mode in ("host", "plan"):
+        sh = to_shard(k, v, 0, N, extra_cap=steps + 2)
+        ws = torch.zeros(M.lib.medha_decode_step_workspace_size(1, h_kv * G, h_kv, d), dtype=torch.uint8, device="cuda")
+        q_h = pin(torch.empty((h_kv * G, d), dtype=torch.bfloat16))
+        k_h = pin(torch.empty((h_kv, d), dtype=torch.bfloat16))
+        v_h = pin(torch.empty((h_kv, d), dtype=torch.bfloat16))
+        o_h = pin(torch.empty((h_kv * G, d), dtype=torch.float32))
+        l_h = pin(torch.empty((h_kv * G,), dtype=torch.float32))
+        plan = M.DecodePlan(c, sh, q_h, k_h, v_h, o_h, l_h, ws) if mode == "plan" else None
+        outs = []
+        for t in range(steps):
+            q_h.copy_(qs[t])
+            k_h.copy_(k[N + t])
+            v_h.copy_(v[N + t])
+            if plan is None:
+                M.decode_step_host(c, sh, True, q_h, k_h, v_h, N + t, o_h, l_h, ws)
+            else:
+                plan.step(sh, True, N + t)
+            torch.cuda.synchronize()
+            outs.append((o_h.clone(), l_h.clone()))
+        if plan is not None:
+            plan.close()
+        assert sh.len == N + steps
+        res.append(outs)
+    for t in range(steps):
+        assert torch.equal(res[0][t][0], res[1][t][0]) and torch.equal(res[0][t][1], res[1][t][1])
+        ro, rl = oracle_attention(qs[t:t + 1], k[:N + t + 1], v[:N + t + 1], [N + t])
+        compare(res[1][t][0][None], res[1][t][1][None], ro, rl, what=f"decode plan step {t}")
