@@ -681,10 +681,15 @@ def main():
     r = bench_decode(args, rank, world, M)
     value = r["bytes_total"] / (r["ms"] * 1e-3) / 1e9
     achieved = r["bytes_rank"] / (r["kern_ms"] * 1e-3) / 1e9
-    traffic = None
+    # DRAM bytes per launch of the decode kernel are not measurable without a profiler: the
+    # value comes from the committed ncu capture named in traffic_source (same kernel, same
+    # configuration), not from this run
+    traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "decode_ncu_traffic.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch", {}).get(f"kvp{world}")
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes_per_launch", {}).get(f"kvp{world}")
+        traffic_src = "profiles/decode_ncu_traffic.json: " + str(tj.get("source_run", tj.get("source", "")))[:160]
     except Exception:
         pass
     extra = {}
@@ -722,7 +727,9 @@ def main():
             "config": _config(world),
             "roofline": {"bound": "hbm", "kernel": "decode_splitkv_kernel<128,4>", "achieved": round(achieved, 1),
                          "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                         "traffic": traffic, "peak_source": peak_src,
+                         "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                         "frac_of_read_probe": (round(achieved / extra["hbm_read_probe_GBps"], 4)
+                                                if extra.get("hbm_read_probe_GBps") else None),
                          "per_launch_bytes": r["bytes_rank"], "kernel_ms": round(r["kern_ms"], 5),
                          "kernel_timing": f"CUDA events around 1 in {r['ev_every']} decode launches of the timed region"},
             "e2e": {"value": round(r["bytes_total"] / (r["e2e_ms"] * 1e-3) / 1e9, 1), "unit": "GB/s",
