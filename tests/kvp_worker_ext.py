@@ -7,6 +7,11 @@
 * N4 KVP x TP, world 4: TP = 2 head slices x KVP = 2 sequence shards; each TP
   slice has its own KVP communicator (torch.distributed sub-group); the concatenated heads
   equal the single-GPU result.
+* N1 / N2 across GPUs: the one-launch KVP step (medha_kvp_decode_append, the tail rank
+  appends) equals append + kvp_decode; medha_kvp_decode captured in a CUDA graph on every
+  rank replays with fresh queries (device-resident epoch) and matches the eager call; and
+  when one rank withholds its pushes (test hook) every rank's bounded wait expires, the
+  communicator reports MEDHA_ENCCL everywhere and nothing hangs.
 """
 import os
 import sys
@@ -71,6 +76,68 @@ def main():
     if seq.active_workers != world:
         fails.append(f"growth reached {seq.active_workers} workers, expected {world}")
     comm.close()
+
+    # ---------------- one-launch step, graph replay, bounded wait --------------------------
+    N = 120_000
+    a0, b0 = shard_range(N, rank, world)
+    tail = rank == world - 1
+    kg = synth.kv_block(51, synth.STREAM_K, 0, N, h_kv, d)
+    vg = synth.kv_block(51, synth.STREAM_V, 0, N, h_kv, d)
+    comm = M.KVPComm()
+    if not comm.p2p:
+        fails.append("fused exchange not initialised")
+    sh_a = to_shard(kg, vg, a0, b0 - 1 if tail else b0, extra_cap=4)
+    sh_b = to_shard(kg, vg, a0, b0 - 1 if tail else b0, extra_cap=4)
+    kn, vn = kg[N - 1:N].cuda(), vg[N - 1:N].cuda()
+    qd = synth.queries(52, 1, h_kv * G, d, amp=6.0).cuda()
+    o1, l1, _ = M.kvp_decode_append(comm, [sh_a], kn, vn, qd, [N - 1], append=[tail])
+    if tail:
+        M.kv_append(sh_b, kn, vn)
+    o2, l2, _ = M.kvp_decode(comm, [sh_b], qd, [N - 1])
+    torch.cuda.synchronize()
+    if (o1 - o2).abs().max().item() > 1e-6:
+        fails.append(f"kvp_decode_append vs append + kvp_decode: {(o1 - o2).abs().max().item()}")
+    allsame(o1, "kvp_decode_append")
+    # CUDA graph replay (every rank replays the same number of times)
+    ws = torch.zeros(M.lib.medha_kvp_workspace_size(world, 1, h_kv * G, h_kv, d), dtype=torch.uint8, device="cuda")
+    q_st = torch.zeros_like(qd)
+    og = torch.empty_like(o1)
+    lg = torch.empty_like(l1)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        M.kvp_decode(comm, [sh_b], q_st, [N - 1], ws=ws, o=og, lse=lg)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        M.kvp_decode(comm, [sh_b], q_st, [N - 1], ws=ws, o=og, lse=lg)
+    for t in range(4):
+        qt = synth.queries(60 + t, 1, h_kv * G, d, amp=6.0).cuda()
+        q_st.copy_(qt)
+        g.replay()
+        torch.cuda.synchronize()
+        oe, le, _ = M.kvp_decode(comm, [sh_b], qt, [N - 1])
+        torch.cuda.synchronize()
+        if not (torch.equal(og, oe) and torch.equal(lg, le)):
+            fails.append(f"graph replay {t} differs from eager kvp_decode")
+    del g
+    dist.barrier()
+    # bounded wait: rank 0 withholds its pushes, everybody must time out and report
+    comm.set_timeout(0.1)
+    if rank == 0:
+        comm.debug(1)
+    ot, lt, _ = M.kvp_decode(comm, [sh_b], qd, [N - 1])
+    torch.cuda.synchronize()
+    if comm.status() != -7:
+        fails.append(f"rank {rank}: status {comm.status()} after a withheld push (expected MEDHA_ENCCL)")
+    try:
+        M.kvp_decode(comm, [sh_b], qd, [N - 1])
+        fails.append("a broken communicator accepted another call")
+    except M.MedhaError:
+        pass
+    comm.close()
+    dist.barrier()
 
     # ---------------- N4: KVP x TP (world 4: 2 x 2) --------------------------------------
     if world == 4:
