@@ -118,6 +118,12 @@ medha_status medha_kv_append(medha_kv_shard *kv, const void *k_new, const void *
  * fixed order inside the same launch (run-to-run deterministic).
  *   kvs_host, q_pos_host: host arrays of length batch (read during the call).
  *   All shards must share h_kv and d; batch <= 4096.
+ * Early start (programmatic dependent launch): the kernel may start streaming K/V rows
+ * [0, len - 1) of each shard, and the query, before the kernel launched just before it on
+ * the stream has completed.  Every kernel of this library allows that only after its own
+ * inputs are final; a foreign kernel that calls
+ * griddepcontrol.launch_dependents / cudaTriggerProgrammaticLaunchCompletion early and
+ * writes those rows or q must not immediately precede this call (or set MEDHA_DEC_EARLY=0).
  */
 size_t medha_decode_workspace_size(int32_t batch, int32_t h_q, int32_t h_kv, int32_t d);
 medha_status medha_attn_decode_partial(const medha_kv_shard *kvs_host, int32_t batch,

@@ -406,7 +406,8 @@ PrefillBatchPlan plan_prefill_batch(const PrefillChunk *ch, int n, int32_t h_q, 
   const double t_tile_us = 1.2;   // ~2 x 1024 MMA clk per KV tile and query pair
   double best = 1e300;
   int64_t best_T = max_tiles;
-  for (int ns = 1; ns <= 64; ++ns) {
+  static const int max_ns = std::max(1, std::min(64, getenv_flag("MEDHA_PF_MAX_SPLITS", 64)));   // A/B knob
+  for (int ns = 1; ns <= max_ns; ++ns) {
     const int64_t T = cdiv(max_tiles, ns);
     if (ns > 1 && T < 4) break;
     int64_t ctas = 0;

@@ -121,3 +121,32 @@ def test_kvp_decode_append_world1(M):
             compare(o2[b:b + 1], l2[b:b + 1], ro, rl, what=f"kvp_decode_append seq {b}")
     finally:
         comm.close()
+
+
+def test_decode_append_batch_over_64(M):
+    """> 64 sequences: two launches on one workspace (both early-started); still equal to
+    kv_append + decode_partial and the appended rows land in every shard."""
+    h_kv, G, d, B = 2, 4, 64, 70
+    rng = np.random.default_rng(11)
+    lens = [int(x) for x in rng.integers(1, 3000, size=B)]
+    ks, vs, a_sh, r_sh = [], [], [], []
+    for b, n in enumerate(lens):
+        k, v = make_global_kv(900 + b, n + 1, h_kv, d)
+        ks.append(k)
+        vs.append(v)
+        a_sh.append(to_shard(k, v, 0, n, extra_cap=2))
+        r_sh.append(to_shard(k, v, 0, n, extra_cap=2))
+    k_new = torch.stack([ks[b][lens[b]] for b in range(B)]).cuda()
+    v_new = torch.stack([vs[b][lens[b]] for b in range(B)]).cuda()
+    q = synth.queries(901, B, h_kv * G, d, amp=4.0).cuda()
+    for b in range(B):
+        M.kv_append(r_sh[b], k_new[b:b + 1], v_new[b:b + 1])
+    o1, l1 = M.attn_decode_partial(r_sh, q, lens)
+    o2, l2 = M.attn_decode_append(a_sh, k_new, v_new, q, lens)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    for b in (0, 63, 64, B - 1):
+        n = lens[b] + 1
+        assert torch.equal(a_sh[b].k[:, :n], r_sh[b].k[:, :n])
+        ro, rl = oracle_attention(q[b:b + 1].cpu(), ks[b], vs[b], [lens[b]])
+        compare(o2[b:b + 1], l2[b:b + 1], ro, rl, what=f"batch>64 seq {b}")
