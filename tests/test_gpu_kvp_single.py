@@ -383,3 +383,48 @@ def test_decode_plan_equals_decode_step_host(M, comm, use_comm, pinned):
         assert torch.equal(res[0][t][0], res[1][t][0]) and torch.equal(res[0][t][1], res[1][t][1])
         ro, rl = oracle_attention(qs[t:t + 1], k[:N + t + 1], v[:N + t + 1], [N + t])
         compare(res[1][t][0][None], res[1][t][1][None], ro, rl, what=f"decode plan step {t}")
+
+
+@pytest.mark.parametrize("tp,kvp", [(2, 2), (4, 2), (2, 4)])
+def test_kvp_x_tp_emulated(M, tp, kvp):
+    """N4 (P:509-516 KVP x TP) on one GPU: TP slices of the KV heads (each with its query heads)
+    times KVP sequence shards; every (slice, rank) partial is a medha_attn_decode_partial /
+    medha_attn_prefill_chunk call, the KVP merge is the K5 kernel over the ranks of a slice,
+    and the slices concatenate to the single-GPU result (north_star 1e-3) and the oracle."""
+    from paper_2409_17264_b200.kvp import shard_range
+    h_kv, G, d, N, c = 8, 4, 128, 40000, 96
+    k, v = make_global_kv(720 + tp * 10 + kvp, N, h_kv, d)
+    qd = synth.queries(721, 1, h_kv * G, d, amp=6.0)
+    qc = synth.queries(722, c, h_kv * G, d, amp=4.0, t0=N - c)
+    whole = to_shard(k, v, 0, N)
+    od1, ld1 = M.attn_decode_partial([whole], qd.cuda(), [N - 1])
+    op1, lp1 = M.attn_prefill_chunk(whole, qc.cuda(), N - c)
+    hs = h_kv // tp
+    od = torch.empty_like(od1)
+    ld = torch.empty_like(ld1)
+    op = torch.empty_like(op1)
+    lp = torch.empty_like(lp1)
+    for t in range(tp):
+        heads = slice(t * hs, (t + 1) * hs)
+        qh = slice(t * hs * G, (t + 1) * hs * G)
+        kt, vt = k[:, heads].contiguous(), v[:, heads].contiguous()
+        parts_d, parts_p = [], []
+        for r in range(kvp):
+            a, b = shard_range(N, r, kvp)
+            sh = to_shard(kt, vt, a, b)
+            o, l = M.attn_decode_partial([sh], qd[:, qh].contiguous().cuda(), [N - 1])
+            parts_d.append(torch.cat([o.reshape(-1), l.reshape(-1)]))
+            o, l = M.attn_prefill_chunk(sh, qc[:, qh].contiguous().cuda(), N - c)
+            parts_p.append(torch.cat([o.reshape(-1), l.reshape(-1)]))
+        o, l, _ = M.merge_partials(torch.stack(parts_d), hs * G, d)
+        od[:, qh], ld[:, qh] = o.view(1, hs * G, d), l.view(1, hs * G)
+        o, l, _ = M.merge_partials(torch.stack(parts_p), c * hs * G, d)
+        op[:, qh], lp[:, qh] = o.view(c, hs * G, d), l.view(c, hs * G)
+    torch.cuda.synchronize()
+    assert (od - od1).abs().max().item() <= KVP_ABS and (ld - ld1).abs().max().item() <= KVP_ABS
+    assert (op - op1).abs().max().item() <= KVP_ABS and (lp - lp1).abs().max().item() <= KVP_ABS
+    ro, rl = oracle_attention(qd, k, v, [N - 1])
+    compare(od, ld, ro, rl, what=f"KVPxTP {tp}x{kvp} decode")
+    rows = [0, c - 1]
+    ro, rl = oracle_attention(qc[rows], k, v, [N - c + r for r in rows])
+    compare(op[rows], lp[rows], ro, rl, what=f"KVPxTP {tp}x{kvp} prefill")
