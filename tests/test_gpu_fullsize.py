@@ -71,6 +71,37 @@ def test_config1_8b_decode_1M(M):
         compare(o[:, h * G:(h + 1) * G], lse[:, h * G:(h + 1) * G], ro, rl, what=f"8B decode 1M head {h}")
 
 
+def test_config1_bench_step_fused_append_1M(M):
+    """configs[1] in the exact launch configuration bench.py times: ONE launch per step that
+    appends the new token (position 2^20 - 1) and decodes over the 2^20 keys, repeated
+    back to back so every launch after the first early-starts under the previous one
+    (PDL); every step must equal the plain decode of the same keys bit for bit, and the
+    oracle on sampled heads."""
+    seed, N, h_kv, G, d = 23, 1 << 20, 8, 4, 128
+    sh = gpu_shard(M, seed, 0, N, h_kv, d)
+    ref = gpu_shard(M, seed, 0, N, h_kv, d)
+    k_new = synth.kv_block(seed, synth.STREAM_K, N - 1, 1, h_kv, d, device="cuda")
+    v_new = synth.kv_block(seed, synth.STREAM_V, N - 1, 1, h_kv, d, device="cuda")
+    sh.k[:, N - 1] = float("nan")            # the slot the append fills: never read before it is written
+    sh.v[:, N - 1] = float("nan")
+    q = synth.queries(seed, 1, h_kv * G, d, amp=6.0).cuda()
+    o_ref, l_ref = M.attn_decode_partial([ref], q, [N - 1])
+    outs = []
+    for _ in range(4):
+        sh.len = N - 1
+        o, lse = M.attn_decode_append([sh], k_new, v_new, q, [N - 1])
+        outs.append((o, lse))
+    torch.cuda.synchronize()
+    for o, lse in outs:
+        assert torch.equal(o, o_ref) and torch.equal(lse, l_ref)
+    assert torch.equal(sh.k[:, N - 1], ref.k[:, N - 1]) and torch.equal(sh.v[:, N - 1], ref.v[:, N - 1])
+    heads = [3]
+    qc = q.cpu()
+    ro, rl = oracle_rows(seed, [qc[:, h * G:(h + 1) * G].double().numpy() for h in heads], [N - 1], heads, N, h_kv,
+                         d)[0]
+    compare(outs[-1][0][:, 3 * G:4 * G], outs[-1][1][:, 3 * G:4 * G], ro, rl, what="bench step 1M head 3")
+
+
 @pytest.mark.parametrize("P0,c", [(1 << 20, 256), (1 << 17, 4096)])
 def test_config2_8b_prefill(M, P0, c):
     """configs[2]: Llama-3 8B chunked prefill at 128K / 1M prefix (sampled rows)."""
