@@ -9,7 +9,7 @@ if [ "${SKIP_PYTEST:-0}" != 1 ]; then
   timeout -s KILL 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -n 2 gpurun_out/pytest_gpu.log
 fi
 timeout -s KILL 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:medha:: -c 400 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-extra --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:decode_splitkv -s 3 -c 1 -f \
   -o gpurun_out/decode_full python bench.py --no-extra --no-cpu --steps 5 --warmup 3 > gpurun_out/ncu_decode.log 2>&1; echo "ncu decode rc=$?"
