@@ -15,7 +15,8 @@ __global__ void kv_append_kernel(const uint4 *__restrict__ k_new, const uint4 *_
                                  const int32_t *__restrict__ pt, int32_t psl,
                                  const uint4 *__restrict__ cp_src, uint4 *__restrict__ cp_dst, int64_t cp_n) {
   // no early trigger: a following decode may read K/V rows (and the staged query) before its
-  // own grid dependency resolves, so it must not start while this kernel writes them
+  // own grid dependency resolves, so it may start only after every CTA has written and fenced
+  // them (the trigger at the end)
   pdl_wait();
 #ifdef MEDHA_DECODE_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0) g_ltrace[g_ltrace_n & 63][3] = gtimer();
@@ -34,6 +35,11 @@ __global__ void kv_append_kernel(const uint4 *__restrict__ k_new, const uint4 *_
     k[dst] = k_new[i];
     v[dst] = v_new[i];
   }
+  // the rows (and the staged query) are performed at gpu scope before a dependent decode
+  // may start its early, pre-wait reads of them
+  __threadfence();
+  __syncthreads();
+  pdl_launch_dependents();
 }
 
 // K5 ("combined using online-softmax"): part r starts at

@@ -91,3 +91,50 @@ def test_fuzz_prefill(M, case):
     rows = sorted(set([0, c - 1] + [int(x) for x in rng.integers(0, c, size=min(c, 6))]))
     ro, rl = oracle_attention(q[rows], k, v, [P0 + r for r in rows], (a, N))
     compare(o[rows], lse[rows], ro, rl, what=f"fuzz prefill {case}: c={c} P0={P0} a={a} G={G} d={d}")
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_fuzz_decode_append_back_to_back(M, case):
+    """Round-2 decode path under fuzzing: several fused append+decode launches back to back on
+    one workspace (each early-starting under the previous one), random group size, head dim,
+    ragged lengths, shard offsets (pos0), append masks and batch sizes; every launch must equal
+    kv_append + decode_partial bit for bit, and sampled sequences the oracle."""
+    import torch
+    rng = np.random.default_rng(7000 + case)
+    d = int(rng.choice([64, 128]))
+    G = int(rng.choice([1, 2, 4, 8, 16]))
+    h_kv = int(rng.choice([1, 2, 4]))
+    B = int(rng.integers(1, 9))
+    steps = 3
+    lens = [int(rng.integers(1, 20000)) for _ in range(B)]
+    starts = [int(rng.integers(0, n)) for n in lens]                  # shard = global tokens [a, N)
+    masks = [[bool(rng.integers(0, 2)) or s == 0 for _ in range(B)] for s in range(steps)]
+    kvs = [make_global_kv(7100 + 10 * case + b, lens[b] + steps, h_kv, d) for b in range(B)]
+    a_sh = [to_shard(kvs[b][0], kvs[b][1], starts[b], lens[b], extra_cap=steps + 1) for b in range(B)]
+    r_sh = [to_shard(kvs[b][0], kvs[b][1], starts[b], lens[b], extra_cap=steps + 1) for b in range(B)]
+    ws = M.decode_workspace(B, h_kv * G, h_kv, d)
+    outs, refs = [], []
+    for s in range(steps):
+        pos = [sh.pos0 + sh.len for sh in a_sh]                       # the next global position
+        k_new = torch.stack([kvs[b][0][pos[b]] for b in range(B)]).cuda()
+        v_new = torch.stack([kvs[b][1][pos[b]] for b in range(B)]).cuda()
+        q = synth.queries(7200 + 10 * case + s, B, h_kv * G, d, amp=float(rng.choice([1.0, 4.0, 8.0]))).cuda()
+        qpos = [pos[b] if masks[s][b] else pos[b] - 1 for b in range(B)]
+        o, lse = M.attn_decode_append(a_sh, k_new, v_new, q, qpos, append=masks[s], ws=ws)
+        outs.append((o, lse, q, qpos, [sh.len for sh in a_sh]))
+    torch.cuda.synchronize()
+    for s in range(steps):
+        o, lse, q, qpos, _ = outs[s]
+        for b in range(B):
+            if masks[s][b]:
+                M.kv_append(r_sh[b], kvs[b][0][r_sh[b].pos0 + r_sh[b].len:][:1].cuda(),
+                            kvs[b][1][r_sh[b].pos0 + r_sh[b].len:][:1].cuda())
+        o1, l1 = M.attn_decode_partial(r_sh, q, qpos)
+        torch.cuda.synchronize()
+        assert torch.equal(o, o1) and torch.equal(lse, l1), f"case {case} step {s}"
+    b = int(rng.integers(0, B))
+    o, lse, q, qpos, lens_after = outs[-1]
+    n_keys = lens_after[b]
+    ro, rl = oracle_attention(q[b:b + 1].cpu(), kvs[b][0], kvs[b][1], [qpos[b]],
+                              (starts[b], starts[b] + n_keys))
+    compare(o[b:b + 1], lse[b:b + 1], ro, rl, what=f"fuzz append {case}/{b}")
