@@ -1,6 +1,6 @@
 """Build libmedha_attn.so in-tree for sm_100a (nvcc, no JIT cache).
 
-    python -m paper_2409_17264_b200.build [--verbose]
+    python paper_2409_17264_b200/build.py [--verbose]   (the package itself needs the .so to import)
 
 The .so lands next to this file, so it travels to the GPU box with the repo
 snapshot.  NCCL comes from the torch-bundled nvidia-nccl wheel (same image on
