@@ -69,3 +69,37 @@ def test_shard_struct_layout_matches_binding(tmp_path):
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
     assert got[0] == ctypes.sizeof(_Shard)
     assert got[1:] == [getattr(_Shard, f).offset for f in fields]
+
+
+def test_argument_errors_are_caught_on_the_host_without_gpu():
+    """Validation that precedes any CUDA call (round-2 entry points included): null or bad
+    arguments return the documented status and a message; nothing is launched."""
+    from paper_2409_17264_b200 import lib, _Shard
+    EINVAL, ERANGE, ENOTSUP, EWS = -1, -3, -4, -5
+    sh = _Shard(0, 0, 100, 10, 0, 8, 128, None, 0, 0, 0)            # null k/v pointers
+    assert lib.medha_kv_append(ctypes.byref(sh), None, None, 1, None) == EINVAL
+    assert b"null" in lib.medha_last_error()
+    qp = (ctypes.c_int64 * 1)(5)
+    assert lib.medha_attn_decode_append(ctypes.byref(sh), 1, None, None, None, None, 32, qp, 0.1, None, None, None,
+                                        0, None) == EINVAL
+    # a well-formed but full shard: the fused append reports ERANGE before launching
+    full = _Shard(16, 16, 100, 100, 0, 8, 128, None, 0, 0, 0)
+    k = (ctypes.c_uint8 * 64)()
+    addr = (ctypes.addressof(k) + 15) // 16 * 16
+    assert lib.medha_attn_decode_append(ctypes.byref(full), 1, addr, addr, None, addr, 32, qp, 0.1, addr, addr, addr,
+                                        1 << 28, None) == ERANGE
+    bad_d = _Shard(16, 16, 100, 10, 0, 8, 96, None, 0, 0, 0)        # head dim 96
+    assert lib.medha_attn_decode_partial(ctypes.byref(bad_d), 1, addr, 32, qp, 0.1, addr, addr, addr, 1 << 28,
+                                         None) == ENOTSUP
+    plan = ctypes.c_void_p()
+    assert lib.medha_decode_plan_create(None, ctypes.byref(sh), 32, 0.1, None, None, None, None, None, None, 0,
+                                        ctypes.byref(plan)) == EINVAL
+    good = _Shard(16, 16, 100, 10, 0, 8, 128, None, 0, 0, 0)
+    assert lib.medha_decode_plan_create(None, ctypes.byref(good), 32, 0.1, addr, None, None, addr, None, addr, 16,
+                                        ctypes.byref(plan)) == EWS
+    assert lib.medha_decode_plan_step(None, ctypes.byref(good), 0, 5, None) == EINVAL
+    assert lib.medha_kvp_comm_status(None) == EINVAL
+    assert lib.medha_kvp_comm_set_timeout(None, 1) == EINVAL
+    assert lib.medha_kvp_comm_debug(None, 1) == EINVAL
+    assert lib.medha_kvp_decode_append(None, ctypes.byref(good), 1, addr, addr, None, addr, 32, qp, 0.1, addr, addr,
+                                       None, addr, 1 << 28, None) == EINVAL
