@@ -59,9 +59,11 @@ def test_decode_append_equals_append_then_decode(M, G, d, lens, mask):
         compare(o2[b:b + 1], l2[b:b + 1], ro, rl, what=f"decode_append seq {b}")
 
 
-def test_decode_append_paged(M):
-    """Paged shard: the owner item stores the new rows through the page table."""
-    h_kv, G, d, ps, n = 2, 4, 128, 64, 5000
+@pytest.mark.parametrize("ps,n", [(64, 5000), (64, 4096), (16, 4095), (256, 1)])
+def test_decode_append_paged(M, ps, n):
+    """Paged shard: the owner item stores the new rows through the page table (incl. a new
+    token that opens a new page, n % ps == 0)."""
+    h_kv, G, d = 2, 4, 128
     rng = np.random.default_rng(7)
     k, v = make_global_kv(620, n + 1, h_kv, d)
     n_pages = (n + 1 + ps - 1) // ps + 1

@@ -52,7 +52,8 @@ def _packed(o, lse):
 
 # ---- a6 + a7 + N1 at world 1 ------------------------------------------------------------
 @pytest.mark.parametrize("G,d,lens", [(4, 128, [40000, 777]), (8, 128, [70000]), (1, 64, [5000, 1, 300]),
-                                      (16, 64, [9000, 20000])])
+                                      (16, 64, [9000, 20000]),
+                                      (4, 64, [int(x) for x in np.random.default_rng(5).integers(1, 3000, 64)])])
 def test_kvp_decode_world1_fused_and_nccl(M, comm, G, d, lens):
     assert comm.world == 1 and comm.p2p, "world-1 fused self-exchange did not initialise"
     h_kv = 2
