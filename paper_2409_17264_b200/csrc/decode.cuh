@@ -213,10 +213,19 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   const int64_t n_vis = S.len_dev ? min64(S.n_vis, *S.len_dev + 1) : S.n_vis;
   const int64_t t_end = min64(t_begin + S.split_tokens, n_vis);
   // fused append: token t_app (-1: none) comes from k_app / v_app
-  int64_t t_app = -1;
-  if (S.k_app) {
-    t_app = S.len_dev ? *S.len_dev : S.t_app;
-    if (t_app >= S.cap) t_app = -1;
+  auto app_token = [&]() -> int64_t {
+    if (!S.k_app) return -1;
+    const int64_t t = S.len_dev ? *S.len_dev : S.t_app;
+    return t < S.cap ? t : -1;
+  };
+  // the appended token is the last visible one (or lies past the split), so the tile holding
+  // it is the split's last tile: the main loop runs to t_bound = that tile's start (all its
+  // tiles are then fully visible) and the tile itself is loaded, patched and computed once
+  // after the loop - no patch code and a single bound in the hot loop (register budget)
+  int64_t t_bound;
+  {
+    const int64_t ta = app_token();
+    t_bound = (ta >= t_begin && ta < t_end) ? (ta & ~15ll) : t_end;
   }
 
   const __nv_bfloat16 *kbase = S.k + (int64_t)kvh * S.hstride * D;
@@ -251,27 +260,43 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   float m_lo = -INFINITY, m_hi = -INFINITY;  // running max (base 2) of rows g, g+8
   float l_lo = 0.f, l_hi = 0.f;              // thread-partial running sums
 
-  const __nv_bfloat16 *kapp = S.k_app ? reinterpret_cast<const __nv_bfloat16 *>(S.k_app) + (int64_t)kvh * D : nullptr;
-  const __nv_bfloat16 *vapp = S.v_app ? reinterpret_cast<const __nv_bfloat16 *>(S.v_app) + (int64_t)kvh * D : nullptr;
   auto load_tile = [&](int64_t tb, uint4 (&kk)[2][KCH], uint4 (&vv)[4][VCH]) {
     const int64_t row0 = tile_row(tb);
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       const int64_t tok = tb + 8 * n + g;
-      const bool ok = tok < t_end;
-      const __nv_bfloat16 *src = (tok == t_app) ? kapp + 8 * c : kbase + (row0 + 8 * n + g) * D + 8 * c;
+      const bool ok = tok < t_bound;
+      const __nv_bfloat16 *src = kbase + (row0 + 8 * n + g) * D + 8 * c;
 #pragma unroll
       for (int i = 0; i < KCH; ++i) kk[n][i] = ok ? ldg_stream(src + 32 * i) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int64_t tok = tb + 2 * c + (r & 1) + 8 * (r >> 1);
-      const bool ok = tok < t_end;
-      const __nv_bfloat16 *src =
-          (tok == t_app) ? vapp + 8 * g : vbase + (row0 + 2 * c + (r & 1) + 8 * (r >> 1)) * D + 8 * g;
+      const bool ok = tok < t_bound;
+      const __nv_bfloat16 *src = vbase + (row0 + 2 * c + (r & 1) + 8 * (r >> 1)) * D + 8 * g;
 #pragma unroll
       for (int i = 0; i < VCH; ++i) vv[r][i] = ok ? ldg_stream(src + 64 * i) : make_uint4(0, 0, 0, 0);
     }
+  };
+
+  // fused append: the tile holding the new token takes that token's fragments from k_new /
+  // v_new (pointers re-read from the kernel parameters); used once per item, after the loop
+  auto patch_app = [&](int64_t tb, int64_t t_app, uint4 (&kk)[2][KCH], uint4 (&vv)[4][VCH]) {
+    const __nv_bfloat16 *kapp = reinterpret_cast<const __nv_bfloat16 *>(S.k_app) + (int64_t)kvh * D;
+    const __nv_bfloat16 *vapp = reinterpret_cast<const __nv_bfloat16 *>(S.v_app) + (int64_t)kvh * D;
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+      if (tb + 8 * n + g == t_app) {
+#pragma unroll
+        for (int i = 0; i < KCH; ++i) kk[n][i] = ldg_stream(kapp + 8 * c + 32 * i);
+      }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (tb + 2 * c + (r & 1) + 8 * (r >> 1) == t_app) {
+#pragma unroll
+        for (int i = 0; i < VCH; ++i) vv[r][i] = ldg_stream(vapp + 8 * g + 64 * i);
+      }
   };
 
   // one 16-token tile: S = QK^T, online softmax, O += PV (K/V fragments in registers)
@@ -295,7 +320,7 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
     for (int n = 0; n < 2; ++n) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const bool ok = (tb + 8 * n + 2 * c + e) < t_end;
+        const bool ok = (tb + 8 * n + 2 * c + e) < t_bound;
         s[n][e] = ok ? s[n][e] * p.scale_log2 : -INFINITY;
         s[n][2 + e] = ok ? s[n][2 + e] * p.scale_log2 : -INFINITY;
         mx_lo = fmaxf(mx_lo, s[n][e]);
@@ -374,32 +399,45 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   int64_t tb = t_begin + 16 * warp;
   // early start: a tile reaching past safe_end (rows the previous kernel may still write)
   // is loaded only after the grid dependency has resolved
-  const int64_t safe_end = S.safe_end;
+  // the bound relative to the split start in one 32-bit register (splits are < 2^31 tokens)
+  const int32_t safe_rel = (int32_t)max64(-1, min64(S.safe_end - t_begin, (int64_t)INT32_MAX));
   auto gate = [&](int64_t t) {
-    if (!waited && t + 16 > safe_end) grid_dep_sync<D, G>(p, sm, waited);
+    if (!waited && (int32_t)(t - t_begin) + 16 > safe_rel) grid_dep_sync<D, G>(p, sm, waited);
   };
 #if MEDHA_DEC_PINGPONG
   // 2x unrolled with ping-pong register buffers: tile i+1 loads while tile i computes,
   // without copying the prefetched fragments between iterations
   uint4 kb0[2][KCH], vb0[4][VCH], kb1[2][KCH], vb1[4][VCH];
-  if (tb < t_end) {
+  if (tb < t_bound) {
     gate(tb);
     load_tile(tb, kb0, vb0);
   }
-  while (tb < t_end) {
-    if (tb + kStep < t_end) {
+  while (tb < t_bound) {
+    if (tb + kStep < t_bound) {
       gate(tb + kStep);
       load_tile(tb + kStep, kb1, vb1);
     }
     compute_tile(kb0, vb0, tb);
     tb += kStep;
-    if (tb >= t_end) break;
-    if (tb + kStep < t_end) {
+    if (tb >= t_bound) break;
+    if (tb + kStep < t_bound) {
       gate(tb + kStep);
       load_tile(tb + kStep, kb0, vb0);
     }
     compute_tile(kb1, vb1, tb);
     tb += kStep;
+  }
+  {
+    // the appended token's tile (bounds recomputed: nothing of this was live in the loop)
+    const int64_t ta = app_token();
+    const int64_t te = min64(t_begin + S.split_tokens, S.len_dev ? min64(S.n_vis, *S.len_dev + 1) : S.n_vis);
+    if (ta >= t_begin && ta < te && (((ta & ~15ll) - t_begin) >> 4) % kDecodeWarps == warp) {
+      t_bound = te;
+      gate(ta & ~15ll);
+      load_tile(ta & ~15ll, kb0, vb0);
+      patch_app(ta & ~15ll, ta, kb0, vb0);
+      compute_tile(kb0, vb0, ta & ~15ll);
+    }
   }
 #else
   uint4 kr[2][KCH], vr[4][VCH];
@@ -427,6 +465,7 @@ __device__ __forceinline__ void decode_item(const DecodeParams &p, const int ite
   grid_dep_sync<D, G>(p, sm, waited);
   // the owner of t_app (its split, or the last split when t_app lies past the visible keys)
   // stores the new K / V rows of this kv head into the shard (never read back in this launch)
+  const int64_t t_app = app_token();
   if (t_app >= 0 && split == (int)min64(t_app / S.split_tokens, S.n_splits - 1) && tid < 2 * (D / 8)) {
     const int64_t row = tile_row(t_app & ~15ll) + (t_app & 15);
     const int e = tid % (D / 8);
